@@ -1,0 +1,149 @@
+/* skr.h -- C ABI of the B200-native SKR hot path (libskr.so).
+ *
+ * Plain pointers, sizes and a cudaStream_t passed as void*; no torch types.
+ * All device pointers must be device-resident (cudaMalloc / torch CUDA tensors).
+ * Compute entry points allocate no device memory: the caller passes a
+ * workspace sized by the *_workspace_bytes() query. Every entry point returns
+ * an int status (SKR_OK = 0); no C++ exception crosses the ABI.
+ *
+ * Reference interfaces replaced (kryrec v0.1.0, /root/reference/pkg/src/kryrec):
+ *   skr_spmv            <- sparse.spmv (sparse.py:155-160) and the operator of
+ *                          gmres.make_operator (gmres.py:184-190) with
+ *                          JacobiPreconditioner.apply (precond.py:66-77)
+ *   skr_gcrodr_solve    <- gcrodr.gcrodr_solve (gcrodr.py:295-496), including
+ *                          refresh_recycle (gcrodr.py:80-113) and the recycle
+ *                          update (gcrodr.py:444-460); k == 0 is the
+ *                          gmres_solve path (gmres.py:193-267, gcrodr.py:326-330)
+ *   skr_sort_dist2 /
+ *   skr_sort_chain      <- sorting.greedy_sort / _greedy_chain (sorting.py:55-80)
+ *   skr_dense_hr_first  <- gcrodr.harmonic_ritz_first_cycle (gcrodr.py:173-206)
+ *   skr_dense_hr_next   <- gcrodr.harmonic_ritz_subsequent (gcrodr.py:209-240)
+ */
+#ifndef SKR_H_
+#define SKR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum skr_status_code {
+  SKR_OK = 0,
+  SKR_ERR_ARG = 1,          /* bad argument (ValueError in the reference) */
+  SKR_ERR_WORKSPACE = 2,    /* workspace too small */
+  SKR_ERR_CUDA = 3,         /* CUDA runtime error */
+  SKR_ERR_TIMEOUT = 4,      /* device barrier / host wait timed out */
+  SKR_ERR_UNSUPPORTED = 5,  /* configuration beyond compiled limits */
+};
+
+/* CSR matrix, int32 indices, fp64 values, device pointers. diag == NULL means
+ * no preconditioner (IdentityPreconditioner); otherwise the Jacobi diagonal
+ * (the left preconditioner M = diag(A), applied as an IEEE division). */
+typedef struct skr_csr {
+  int32_t n;
+  int32_t nnz;
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  const double* values;
+  const double* diag;
+} skr_csr;
+
+/* SolverConfig (gmres.py:26-43). */
+typedef struct skr_config {
+  int32_t m;
+  int32_t k;
+  int32_t max_iter;
+  int32_t reserved;
+  double tol;
+} skr_config;
+
+/* SolveReport (gmres.py:46-56) minus the vectors. */
+typedef struct skr_report {
+  int32_t iterations;
+  int32_t converged;
+  int32_t k_out;          /* recycle columns on exit (0 = empty space) */
+  int32_t hist_len;       /* residual_history length */
+  int32_t n_checks;       /* restart_checks entries */
+  int32_t deflated_steps;
+  int32_t warn_bits;      /* reference warnings.warn equivalents, see skr_warn */
+  int32_t status_bits;    /* internal dense-kernel status (informational) */
+  int32_t zero_rhs;       /* b == 0 early return (gcrodr.py:337-346) */
+  int32_t gmres_fallback; /* U stayed None (gcrodr.py:481-483) */
+  int32_t cycles;
+  int32_t reserved;
+  double true_relative_residual;
+  double rnorm;
+  double abs_tol;
+  double bnorm;
+  double device_ms;       /* device time of the solve (CUDA events) */
+  double spmv_ortho_bytes;/* algorithmic bytes of the Arnoldi steps */
+} skr_report;
+
+enum skr_warn {
+  SKR_WARN_SINGULAR_H = 1,
+  SKR_WARN_SINGULAR_CROSS = 2,
+  SKR_WARN_RANK_DROP = 4,
+  SKR_WARN_REFRESH_RANK = 8,
+  SKR_WARN_JACOBI_SVD = 16,
+};
+
+int skr_version(void);
+const char* skr_status_string(int status);
+/* number of SMs / L2 bytes of the current device (for reports) */
+int skr_device_info(int* sm_count, long long* l2_bytes);
+
+/* y = A x, or y = D^-1 (A x) when apply_prec and A->diag. Bit-exact with
+ * scipy's csr_matvec (sequential row sum from 0.0, no FMA) + numpy divide. */
+int skr_spmv(const skr_csr* A, const double* x, double* y, int apply_prec, void* stream);
+/* r = D^-1 (b - A x) (or b - A x): the reference's explicit residual. */
+int skr_residual(const skr_csr* A, const double* b, const double* x, double* r, int apply_prec,
+                 void* stream);
+
+size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter);
+/* Solve A x = b with GCRO-DR. U_in (n x k_in, column-major, leading dim ldu)
+ * is the previous system's recycle U (its C is not needed: the refresh
+ * discards it, gcrodr.py:361-366); U_in may alias the workspace's own U block
+ * (chain mode, see skr_gcrodr_recycle_view). x0 may be NULL. x is written.
+ * hist/checks (host, may be NULL) receive residual_history and
+ * restart_checks (pairs). */
+int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double* x,
+                     const skr_config* cfg, const double* U_in, int32_t ldu, int32_t k_in,
+                     void* workspace, size_t ws_bytes, skr_report* report, double* hist,
+                     int32_t hist_cap, double* checks, int32_t checks_cap, void* stream);
+/* Device pointers of the recycle pair left in the workspace by the last solve:
+ * U (n x k, ld) and C (n x k, ld). */
+int skr_gcrodr_recycle_view(void* workspace, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
+                            double** U, double** C, int32_t* k_out, int32_t* ld);
+
+/* Greedy nearest-neighbour sort. params: n_sys x P row-major fp64 (device).
+ * dist2 fills D2[i - row0][j] = ||p_i - p_j||^2 for i in [row0, row1), all j
+ * (binary {v0, v1} batches use an exact bit-count path). chain computes the
+ * order from the full D2 (n_sys x n_sys) with the reference's tie-break and a
+ * certified argmin: near-ties are re-evaluated in the reference's exact
+ * arithmetic (numpy pairwise summation). */
+size_t skr_sort_workspace_bytes(int32_t n_sys, int64_t P);
+int skr_sort_binary_check(const double* params, int32_t n_sys, int64_t P, double* v0v1,
+                          int32_t* is_binary, void* workspace, size_t ws_bytes, void* stream);
+int skr_sort_dist2(const double* params, int32_t n_sys, int64_t P, int32_t row0, int32_t row1,
+                   int32_t binary, double v0, double v1, double* D2, void* workspace,
+                   size_t ws_bytes, void* stream);
+int skr_sort_chain(const double* D2, const double* params, int32_t n_sys, int64_t P,
+                   int32_t exact_d2, int32_t* order, int32_t* n_certified, void* stream);
+/* one-call single-GPU greedy_sort (sorting.py:72-80) */
+int skr_greedy_sort(const double* params, int32_t n_sys, int64_t P, int32_t* order_host,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* Single-CTA dense steps on the device (test / diagnostic entry points).
+ * H: (m+1) x m column-major (ld), G: (mm+1) x mm, cross: mm x mm. P out:
+ * ld_p x cols, returns the number of columns in *ncols (or negative status). */
+int skr_dense_hr_first(const double* H, int32_t ldh, int32_t m, int32_t k, double* P,
+                       int32_t ldp, int32_t* ncols, void* stream);
+int skr_dense_hr_next(const double* G, int32_t ldg, const double* cross, int32_t ldx, int32_t mm,
+                      int32_t k, double* P, int32_t ldp, int32_t* ncols, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKR_H_ */

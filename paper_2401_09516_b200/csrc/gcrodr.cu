@@ -1,0 +1,1541 @@
+// GCRO-DR solve for one sparse fp64 system on a B200, with the recycle pair
+// carried between systems (kryrec/gcrodr.py:295-496 restated for the GPU).
+//
+// Kernels (one stream, no host sync inside a cycle):
+//   k_setup / k_init           scalars, x0, r = M^-1 b, norms (gcrodr.py:332-353)
+//   refresh chain              CholQR2 of U_in, W = op(Yo), CholQR2 + QRCP of W,
+//                              U = Yo[:, kept] R^-1, projection (gcrodr.py:80-113, 360-378)
+//   k_cycle (cooperative)      ONE launch per restart cycle: the whole deflated (or
+//                              first GMRES) Arnoldi cycle with lagged one-reduction
+//                              CGS2 (DCGS2: sweep 1 = SpMV + multi-dot, one grid
+//                              reduction, sweep 2 = finishing AXPYs), Givens LS in
+//                              every CTA, x update, explicit residual and the
+//                              cross-Gram for the recycle update (gcrodr.py:398-448)
+//   k_dense (1 CTA)            harmonic Ritz + QRCP recycle update, state machine
+//                              (gcrodr.py:444-470, 280-292, dense.h / recycle.h)
+//   k_combine                  U, C <- [U | C | V] coefficients, in place, row-parallel
+// The host loop enqueues cycles ahead and polls a mapped flag the dense kernel
+// writes, so the GPU never waits for the CPU.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <thread>
+
+#include "recycle.h"
+#include "skr_device.cuh"
+
+namespace skr {
+
+// ---------------------------------------------------------------------------
+// device state
+// ---------------------------------------------------------------------------
+constexpr int LDH = MMAX + 1;          // ld of H (rows <= m+1)
+constexpr int LDR = MMAX;              // ld of rotated R
+constexpr int LDB = KMAX;              // ld of B
+constexpr int LDX = MMAX;              // ld of cross
+constexpr int LDC = KMAX + MMAX + 1;   // ld of coefficient matrices
+constexpr int LDK = KMAX;              // ld of small k x k matrices
+
+enum Prog {
+  P_INIT = 0,
+  P_CHOL1 = 1,   // CholQR pass 1 on a tall block (arg: 0 = U block, 1 = C block)
+  P_CHOL2 = 2,   // pass 2 + QRCP(R) ; arg 0 = orth(U) ; arg 1 = QR(W) -> C, U
+  P_PROJ_FIN = 3,
+  P_CYCLE = 4,
+  P_FINAL = 5,
+};
+
+enum CombineMode {
+  CM_CYCLE = 0,     // U, C <- [U|V] coefU, [C|V] coefC (recycle update)
+  CM_U_ONLY = 1,    // U[:, :nout] <- U[:, :nin] T
+  CM_C_ONLY = 2,    // C <- C T
+  CM_REFRESH = 3,   // C <- C Tc ; U <- U Tu
+};
+
+struct State {
+  // config
+  int n, ld, m, k, kcap, max_iter, jacobi, nblk, rpb, k_in, has_x0, pad0;
+  double tol;
+  // scalars
+  double bnorm, bprec, abs_tol, rnorm, true_rel;
+  int iters, kc, kc_prev, k_new, converged, done, brk, ran, upd, j, cycles, defl_steps;
+  int hist_len, nchecks, warn, status, abort_flag, zero_rhs, fallback, ncol_a, ncol_b, r_tmp,
+      cm_mode, cm_nin_u, cm_nin_c, cm_nv, cm_nout_u, cm_nout_c, ncol_orig;
+  unsigned bar_count, bar_gen;
+  int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
+  double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
+  int kept[KMAX];
+  // per-cycle small data
+  double H[LDH * MMAX];
+  double B[LDB * MMAX];
+  double R[LDR * MMAX];
+  double g[MMAX + 1];
+  double y[KMAX + MMAX];
+  double dk[KMAX];
+  double cr[KMAX];
+  double cross[LDX * MMAX];
+  double coefU[LDC * KMAX];
+  double coefC[LDC * KMAX];
+  double gram[LDK * KMAX];
+  double R1[LDK * KMAX];
+  double alpha[KMAX];
+  double red[PV_STEP];
+};
+
+struct Layout {
+  size_t state, basis, r, z, part, hist, checks, total;
+  int ld, kcap, ncols, hist_cap;
+};
+
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static Layout make_layout(int n, int m, int k, int max_iter) {
+  Layout L;
+  L.ld = (int)align_up((size_t)std::max(n, 1), 64);
+  L.kcap = k + 1;
+  L.ncols = 2 * L.kcap + m + 1;
+  L.hist_cap = max_iter + 2 * L.kcap + 8;
+  size_t off = 0;
+  L.state = off;
+  off = align_up(off + sizeof(State), 256);
+  L.basis = off;
+  off = align_up(off + (size_t)L.ld * L.ncols * sizeof(double), 256);
+  L.r = off;
+  off = align_up(off + (size_t)L.ld * sizeof(double), 256);
+  L.z = off;
+  off = align_up(off + (size_t)L.ld * sizeof(double), 256);
+  L.part = off;
+  off = align_up(off + (size_t)(PV_MAX + 16) * GRID_MAX * sizeof(double), 256);
+  L.hist = off;
+  off = align_up(off + (size_t)L.hist_cap * sizeof(double), 256);
+  L.checks = off;
+  off = align_up(off + (size_t)2 * L.hist_cap * sizeof(double), 256);
+  L.total = off;
+  return L;
+}
+
+struct Ptrs {
+  State* st;
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* av;
+  const double* dg;  // Jacobi diagonal or nullptr
+  const double* b;
+  double* x;
+  double* r;
+  double* z;
+  double* basis;
+  double* part;
+  double* hist;
+  double* checks;
+  int n, ld, kcap, nblk, rpb;
+};
+
+__device__ __forceinline__ double* colU(const Ptrs& p, int c) { return p.basis + (size_t)c * p.ld; }
+// C block column c in [0, kcap): global column kcap + c; active C = last kc.
+__device__ __forceinline__ double* colC(const Ptrs& p, int c) {
+  return p.basis + (size_t)(p.kcap + c) * p.ld;
+}
+__device__ __forceinline__ double* colV(const Ptrs& p, int v) {
+  return p.basis + (size_t)(2 * p.kcap + v) * p.ld;
+}
+
+__device__ __forceinline__ void flag_host(State* st, int cycle, int done) {
+  if (st->host_flag) {
+    volatile int* hf = st->host_flag;
+    hf[1] = done;
+    __threadfence_system();
+    hf[0] = cycle;
+    __threadfence_system();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// setup / init
+// ---------------------------------------------------------------------------
+__global__ void k_setup(State* st, int n, int ld, int m, int k, int max_iter, double tol,
+                        int jacobi, int nblk, int rpb, int k_in, int has_x0, int* host_flag) {
+  // zero the scalar header (everything before kept[])
+  char* p = reinterpret_cast<char*>(st);
+  size_t hdr = offsetof(State, kept);
+  for (size_t i = threadIdx.x; i < hdr; i += blockDim.x) p[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->n = n;
+    st->ld = ld;
+    st->m = m;
+    st->k = k;
+    st->kcap = k + 1;
+    st->max_iter = max_iter;
+    st->tol = tol;
+    st->jacobi = jacobi;
+    st->nblk = nblk;
+    st->rpb = rpb;
+    st->k_in = k_in;
+    st->has_x0 = has_x0;
+    st->host_flag = host_flag;
+    if (host_flag) {
+      host_flag[0] = -1;
+      host_flag[1] = 0;
+    }
+  }
+}
+
+// x = x0 or 0; r = M^-1 (b - A x) or M^-1 b; partials: |b|^2, |M^-1 b|^2, |r|^2
+__global__ void __launch_bounds__(NT) k_init(Ptrs p, const double* x0) {
+  __shared__ double s_red[NW];
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  double sb = 0.0, sbp = 0.0, sr = 0.0;
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    double bv = __ldg(p.b + row);
+    double xv = x0 ? x0[row] : 0.0;
+    p.x[row] = xv;
+    double bp = p.dg ? __ddiv_rn(bv, __ldg(p.dg + row)) : bv;
+    sb += bv * bv;
+    sbp += bp * bp;
+  }
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    double bv = __ldg(p.b + row);
+    double rv;
+    if (x0) {
+      double t = csr_row(p.rp, p.ci, p.av, x0, row);
+      rv = __dsub_rn(bv, t);
+    } else {
+      rv = bv;
+    }
+    if (p.dg) rv = __ddiv_rn(rv, __ldg(p.dg + row));
+    p.r[row] = rv;
+    sr += rv * rv;
+  }
+  double t0 = block_sum(sb, s_red);
+  double t1 = block_sum(sbp, s_red);
+  double t2 = block_sum(sr, s_red);
+  if (threadIdx.x == 0) {
+    p.part[0 * GRID_MAX + blockIdx.x] = t0;
+    p.part[1 * GRID_MAX + blockIdx.x] = t1;
+    p.part[2 * GRID_MAX + blockIdx.x] = t2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic partial producers for the refresh
+// ---------------------------------------------------------------------------
+// Gram partials X^T X of nc columns starting at column pointer base (stride
+// ld) -> part[(i*nc + j) * GRID_MAX + blk]
+__global__ void __launch_bounds__(NT) k_gram(Ptrs p, int which, int ncols_from_state) {
+  State* st = p.st;
+  if (st->done) return;
+  int nc = ncols_from_state == 0 ? st->ncol_a : st->ncol_b;
+  if (nc <= 0) return;
+  const double* base = which == 0 ? colU(p, 0) : colC(p, p.kcap - nc);
+  __shared__ double tile[32][KMAX + 1];
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  int ne = nc * nc;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // ne <= 1024 = 4 * NT
+  for (int t0 = r0; t0 < r1; t0 += 32) {
+    for (int e = threadIdx.x; e < 32 * nc; e += NT) {
+      int rr = e % 32, c = e / 32;
+      int row = t0 + rr;
+      tile[rr][c] = row < r1 ? base[(size_t)c * p.ld + row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int e = threadIdx.x + q * NT;
+      if (e < ne) {
+        int i = e % nc, j = e / nc;
+        double s = 0.0;
+        for (int rr = 0; rr < 32; ++rr) s += tile[rr][i] * tile[rr][j];
+        acc[q] += s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int e = threadIdx.x + q * NT;
+    if (e < ne) p.part[(size_t)e * GRID_MAX + blockIdx.x] = acc[q];
+  }
+}
+
+// C^T r partials (kc values) for the projection after the refresh
+__global__ void __launch_bounds__(NT) k_ctr(Ptrs p) {
+  State* st = p.st;
+  if (st->done || st->kc == 0) return;
+  int kc = st->kc;
+  __shared__ double s_red[NW];
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  for (int c = 0; c < kc; ++c) {
+    const double* C = colC(p, p.kcap - kc + c);
+    double s = 0.0;
+    for (int row = r0 + threadIdx.x; row < r1; row += NT) s += C[row] * p.r[row];
+    double t = block_sum(s, s_red);
+    if (threadIdx.x == 0) p.part[(size_t)c * GRID_MAX + blockIdx.x] = t;
+  }
+}
+
+// Deterministic reduction of nv partial values into dst (state arrays).
+__global__ void __launch_bounds__(NT) k_reduce(Ptrs p, int nv_from, int dst) {
+  State* st = p.st;
+  if (st->done) return;
+  int nv;
+  double* out;
+  switch (nv_from) {
+    case 0: nv = st->ncol_a * st->ncol_a; out = st->gram; break;       // gram of U block
+    case 1: nv = st->ncol_b * st->ncol_b; out = st->gram; break;       // gram of C block
+    default: nv = st->kc; out = st->alpha; break;                      // C^T r
+  }
+  (void)dst;
+  if (nv <= 0) return;
+  int lane = threadIdx.x & 31;
+  int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
+  int nwt = (gridDim.x * NT) >> 5;
+  for (int v = gw; v < nv; v += nwt) {
+    const double* q = p.part + (size_t)v * GRID_MAX;
+    double s = 0.0;
+    for (int b = lane; b < p.nblk; b += 32) s += q[b];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (nv_from <= 1) {
+        int nc = (nv_from == 0) ? st->ncol_a : st->ncol_b;
+        out[(v % nc) + (v / nc) * LDK] = s;
+      } else {
+        out[v] = s;
+      }
+    }
+  }
+}
+
+// W = op(Yo): C block (last r columns) <- M^-1 A U[:, :r]
+__global__ void __launch_bounds__(NT) k_spmm(Ptrs p) {
+  State* st = p.st;
+  if (st->done) return;
+  int r = st->ncol_a;
+  if (r <= 0) return;
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    int s = __ldg(p.rp + row), e = __ldg(p.rp + row + 1);
+    double d = p.dg ? __ldg(p.dg + row) : 1.0;
+    for (int c = 0; c < r; ++c) {
+      const double* Y = colU(p, c);
+      double acc = 0.0;
+      for (int q = s; q < e; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(p.av + q), Y[__ldg(p.ci + q)]));
+      if (p.dg) acc = __ddiv_rn(acc, d);
+      colC(p, p.kcap - r + c)[row] = acc;
+    }
+  }
+}
+
+// x += U alpha ; r -= C alpha ; partials: C^T r_new (kc), |U_c|^2 (kc), |r_new|^2
+__global__ void __launch_bounds__(NT) k_project(Ptrs p) {
+  State* st = p.st;
+  if (st->done || st->kc == 0) return;
+  int kc = st->kc;
+  __shared__ double s_al[KMAX];
+  __shared__ double s_red[NW];
+  if (threadIdx.x < kc) s_al[threadIdx.x] = st->alpha[threadIdx.x];
+  __syncthreads();
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  double rr = 0.0;
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    double ua = 0.0, ca = 0.0;
+    for (int c = 0; c < kc; ++c) {
+      ua += colU(p, c)[row] * s_al[c];
+      ca += colC(p, p.kcap - kc + c)[row] * s_al[c];
+    }
+    p.x[row] = p.x[row] + ua;
+    double rv = p.r[row] - ca;
+    p.r[row] = rv;
+    rr += rv * rv;
+  }
+  __syncthreads();
+  for (int c = 0; c < kc; ++c) {
+    const double* C = colC(p, p.kcap - kc + c);
+    const double* U = colU(p, c);
+    double s1 = 0.0, s2 = 0.0;
+    for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+      s1 += C[row] * p.r[row];
+      double u = U[row];
+      s2 += u * u;
+    }
+    double t1 = block_sum(s1, s_red);
+    double t2 = block_sum(s2, s_red);
+    if (threadIdx.x == 0) {
+      p.part[(size_t)c * GRID_MAX + blockIdx.x] = t1;
+      p.part[(size_t)(kc + c) * GRID_MAX + blockIdx.x] = t2;
+    }
+  }
+  double t = block_sum(rr, s_red);
+  if (threadIdx.x == 0) p.part[(size_t)(2 * kc) * GRID_MAX + blockIdx.x] = t;
+}
+
+// true residual partials |b - A x|^2
+__global__ void __launch_bounds__(NT) k_final_resid(Ptrs p) {
+  __shared__ double s_red[NW];
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  double s = 0.0;
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    double t = __dsub_rn(__ldg(p.b + row), csr_row(p.rp, p.ci, p.av, p.x, row));
+    s += t * t;
+  }
+  double t = block_sum(s, s_red);
+  if (threadIdx.x == 0) p.part[blockIdx.x] = t;
+}
+
+// ---------------------------------------------------------------------------
+// combine: row-parallel small-coefficient update of U / C, in place
+// ---------------------------------------------------------------------------
+template <int KT>
+__global__ void __launch_bounds__(NT) k_combine(Ptrs p, int cycle_mode) {
+  State* st = p.st;
+  if (cycle_mode) {
+    if (!st->ran) return;
+  } else if (st->done) {
+    return;
+  }
+  extern __shared__ double sm[];
+  int mode = cycle_mode ? CM_CYCLE : st->cm_mode;
+  int nin_u, nin_c, nv, nout_u, nout_c;
+  const double* cu;
+  const double* cc;
+  int ldcu, ldcc;
+  if (mode == CM_CYCLE) {
+    nin_u = st->kc_prev;
+    nin_c = st->kc_prev;
+    nv = st->j;  // U uses V_0..V_{j-1}; C uses V_0..V_j
+    nout_u = st->upd ? st->k_new : 0;
+    nout_c = nout_u;
+    cu = st->coefU;
+    cc = st->coefC;
+    ldcu = LDC;
+    ldcc = LDC;
+  } else {
+    nin_u = st->cm_nin_u;
+    nin_c = st->cm_nin_c;
+    nv = 0;
+    nout_u = st->cm_nout_u;
+    nout_c = st->cm_nout_c;
+    cu = st->coefU;
+    cc = st->coefC;
+    ldcu = LDC;
+    ldcc = LDC;
+  }
+  int rows_u = nin_u + nv, rows_c = nin_c + (mode == CM_CYCLE ? nv + 1 : 0);
+  double* s_cu = sm;                       // rows_u x nout_u
+  double* s_cc = sm + (size_t)LDC * KT;    // rows_c x nout_c
+  __shared__ double s_red[NW];
+  for (int e = threadIdx.x; e < rows_u * nout_u; e += NT)
+    s_cu[(e % rows_u) + (e / rows_u) * LDC] = cu[(e % rows_u) + (e / rows_u) * ldcu];
+  for (int e = threadIdx.x; e < rows_c * nout_c; e += NT)
+    s_cc[(e % rows_c) + (e / rows_c) * LDC] = cc[(e % rows_c) + (e / rows_c) * ldcc];
+  __syncthreads();
+  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  int cbase_in = p.kcap - nin_c;
+  int cbase_out = p.kcap - nout_c;
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    double au[KT], ac[KT];
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      au[q] = 0.0;
+      ac[q] = 0.0;
+    }
+    if (nout_u > 0)
+      for (int c = 0; c < nin_u; ++c) {
+        double v = colU(p, c)[row];
+#pragma unroll
+        for (int q = 0; q < KT; ++q)
+          if (q < nout_u) au[q] += v * s_cu[c + q * LDC];
+      }
+    if (nout_c > 0)
+      for (int c = 0; c < nin_c; ++c) {
+        double v = colC(p, cbase_in + c)[row];
+#pragma unroll
+        for (int q = 0; q < KT; ++q)
+          if (q < nout_c) ac[q] += v * s_cc[c + q * LDC];
+      }
+    if (mode == CM_CYCLE && (nout_u > 0 || nout_c > 0)) {
+      for (int v = 0; v <= nv; ++v) {
+        double x = colV(p, v)[row];
+        if (v < nv)
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < nout_u) au[q] += x * s_cu[nin_u + v + q * LDC];
+#pragma unroll
+        for (int q = 0; q < KT; ++q)
+          if (q < nout_c) ac[q] += x * s_cc[nin_c + v + q * LDC];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      if (q < nout_u) colU(p, q)[row] = au[q];
+      if (q < nout_c) colC(p, cbase_out + q)[row] = ac[q];
+    }
+  }
+  if (mode == CM_CYCLE && !st->done) {
+    // partials for the next cycle start: C^T r (kc) and |U_c|^2 (kc)
+    int kc = st->kc;
+    __syncthreads();
+    for (int c = 0; c < kc; ++c) {
+      const double* C = colC(p, p.kcap - kc + c);
+      const double* U = colU(p, c);
+      double s1 = 0.0, s2 = 0.0;
+      for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+        s1 += C[row] * p.r[row];
+        double u = U[row];
+        s2 += u * u;
+      }
+      double t1 = block_sum(s1, s_red);
+      double t2 = block_sum(s2, s_red);
+      if (threadIdx.x == 0) {
+        p.part[(size_t)c * GRID_MAX + blockIdx.x] = t1;
+        p.part[(size_t)(kc + c) * GRID_MAX + blockIdx.x] = t2;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the persistent Arnoldi-cycle kernel
+// ---------------------------------------------------------------------------
+struct CycleSmem {
+  double w[NT];
+  double z[NT];
+  double red[PV_STEP];
+  double a[KMAX + MMAX];     // reorthogonalisation coefficients of the pending vector
+  double bb[KMAX + MMAX];    // first-pass coefficients of the new vector (scaled)
+  double cs[MMAX], sn[MMAX], gv[MMAX + 1];
+  double hp[MMAX + 1];       // first-pass H column of the pending vector
+  double bp[KMAX];           // first-pass B column
+  double dk[KMAX], cr[KMAX];
+  double y[KMAX + MMAX];
+  double sc[16];             // scalars
+  double bred[NW];
+  int flag;
+};
+
+#define CYCLE_SYNC()                                              \
+  do {                                                            \
+    if (!grid_sync(bc, bg, abt, nblk, &S.flag)) {                 \
+      if (tid == 0) {                                             \
+        st->done = 1;                                             \
+        if (blk == 0) flag_host(st, cycle_id, 1);                 \
+      }                                                           \
+      return;                                                     \
+    }                                                             \
+  } while (0)
+
+__global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
+  State* st = p.st;
+  __shared__ CycleSmem S;
+  __shared__ double gtile[16][KMAX * 2 + MMAX + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int blk = blockIdx.x, nblk = p.nblk;
+  if (st->done) {
+    if (blk == 0 && tid == 0) st->ran = 0;
+    return;
+  }
+  const int n = p.n;
+  const int kc = st->kc;
+  const bool defl = kc > 0;
+  const int m = st->m;
+  const int kcap = p.kcap;
+  int budget = st->max_iter - st->iters;
+  int s = defl ? max(1, m - kc) : m;
+  s = min(s, budget);
+  const double abs_tol = st->abs_tol;
+  const double beta = st->rnorm;
+  const int r0 = blk * p.rpb, r1 = min(n, r0 + p.rpb);
+  double* Qb = colC(p, kcap - kc);  // [C | V_0 ...] contiguous
+  const size_t ld = p.ld;
+  unsigned* bc = &st->bar_count;
+  unsigned* bg = &st->bar_gen;
+  int* abt = &st->abort_flag;
+
+  // ---- cycle start --------------------------------------------------------
+  if (defl) {
+    reduce_partials(p.part, GRID_MAX, nblk, 0, 2 * kc, S.red);
+    if (tid < kc) {
+      double u2 = S.red[kc + tid];
+      double un = sqrt(u2);
+      S.dk[tid] = un == 0.0 ? 1.0 : 1.0 / un;
+      S.cr[tid] = S.red[tid];
+    }
+  }
+  if (tid == 0) S.gv[0] = beta;
+  {
+    double* V0 = colV(p, 0);
+    for (int row = r0 + tid; row < r1; row += NT) V0[row] = p.r[row] / beta;
+  }
+  if (blk == 0 && tid < kc) {
+    st->dk[tid] = S.dk[tid];
+    st->cr[tid] = S.cr[tid];
+  }
+  CYCLE_SYNC();
+
+  int j = 0;
+  bool brk = false;
+  double wn0_pending = 0.0;  // ||w - C C^T w|| / eta of the pending vector's step
+  double hres = beta;
+  for (int t = 0; t <= s; ++t) {
+    const bool do_spmv = (t < s);
+    const int pb = kc + t;  // final basis columns [C | v_0..v_{t-1}]
+    double* Vt = colV(p, t);
+    // ---- sweep 1: z = op(V_t); dots of V_t and z against the final basis --
+    double acc_a[QMAX], acc_b[QMAX];
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      acc_a[q] = 0.0;
+      acc_b[q] = 0.0;
+    }
+    double nu = 0.0, mu = 0.0, ze = 0.0;
+    for (int t0 = r0; t0 < r1; t0 += NT) {
+      int row = t0 + tid;
+      double wv = 0.0, zv = 0.0;
+      if (row < r1) {
+        wv = Vt[row];
+        if (do_spmv) {
+          zv = csr_row(p.rp, p.ci, p.av, Vt, row);
+          if (p.dg) zv = __ddiv_rn(zv, __ldg(p.dg + row));
+          p.z[row] = zv;
+        }
+      }
+      nu += wv * wv;
+      mu += wv * zv;
+      ze += zv * zv;
+      S.w[tid] = wv;
+      S.z[tid] = zv;
+      __syncthreads();
+      int nrow = min(NT, r1 - t0);
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        int col = warp + q * NW;
+        if (col < pb) {
+          const double* Qc = Qb + (size_t)col * ld + t0;
+          double sa = 0.0, sb = 0.0;
+#pragma unroll 4
+          for (int rr = lane; rr < nrow; rr += 32) {
+            double qv = Qc[rr];
+            sa += qv * S.w[rr];
+            sb += qv * S.z[rr];
+          }
+          acc_a[q] += sa;
+          acc_b[q] += sb;
+        }
+      }
+      __syncthreads();
+    }
+    // partial layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      int col = warp + q * NW;
+      double sa = acc_a[q], sb = acc_b[q];
+      for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+      if (col < pb && lane == 0) {
+        p.part[(size_t)(3 + col) * GRID_MAX + blk] = sa;
+        p.part[(size_t)(3 + pb + col) * GRID_MAX + blk] = sb;
+      }
+    }
+    {
+      double t_nu = block_sum(nu, S.bred);
+      double t_mu = block_sum(mu, S.bred);
+      double t_ze = block_sum(ze, S.bred);
+      if (tid == 0) {
+        p.part[0 * GRID_MAX + blk] = t_nu;
+        p.part[1 * GRID_MAX + blk] = t_mu;
+        p.part[2 * GRID_MAX + blk] = t_ze;
+      }
+    }
+    CYCLE_SYNC();
+    reduce_partials(p.part, GRID_MAX, nblk, 0, 3 + 2 * pb, S.red);
+    // ---- LS / control (identical in every CTA) ------------------------------
+    if (tid == 0) {
+      double nu_ = S.red[0], mu_ = S.red[1], ze_ = S.red[2];
+      const double* A_ = S.red + 3;
+      const double* BB = S.red + 3 + pb;
+      bool stop = false;
+      double eta = 1.0;
+      if (t >= 1) {
+        double aa = 0.0;
+        for (int c = 0; c < pb; ++c) aa += A_[c] * A_[c];
+        eta = sqrt(fmax(nu_ - aa, 0.0));
+        int i = t - 1;  // finalize column i
+        double hcol[MMAX + 1];
+        for (int q = 0; q <= i; ++q) hcol[q] = S.hp[q] + A_[kc + q];
+        hcol[i + 1] = eta;
+        brk = eta < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308);
+        if (blk == 0) {
+          for (int c = 0; c < kc; ++c) st->B[c + i * LDB] = S.bp[c] + A_[c];
+          for (int q = 0; q <= i + 1; ++q) st->H[q + i * LDH] = hcol[q];
+          for (int q = i + 2; q < LDH; ++q) st->H[q + i * LDH] = 0.0;
+        }
+        // Givens
+        for (int q = 0; q < i; ++q) {
+          double tt = S.cs[q] * hcol[q] + S.sn[q] * hcol[q + 1];
+          hcol[q + 1] = -S.sn[q] * hcol[q] + S.cs[q] * hcol[q + 1];
+          hcol[q] = tt;
+        }
+        double den = hypot(hcol[i], hcol[i + 1]);
+        double cs_, sn_;
+        if (den == 0.0) {
+          cs_ = 1.0;
+          sn_ = 0.0;
+        } else {
+          cs_ = hcol[i] / den;
+          sn_ = hcol[i + 1] / den;
+        }
+        S.cs[i] = cs_;
+        S.sn[i] = sn_;
+        hcol[i] = den;
+        S.gv[i + 1] = -sn_ * S.gv[i];
+        S.gv[i] = cs_ * S.gv[i];
+        hres = fabs(S.gv[i + 1]);
+        if (blk == 0) {
+          for (int q = 0; q <= i; ++q) st->R[q + i * LDR] = hcol[q];
+          p.hist[st->hist_len + i] = hres;
+        }
+        stop = brk || hres <= abs_tol || t == s;
+      }
+      S.sc[0] = eta;
+      S.sc[1] = stop ? 1.0 : 0.0;
+      S.sc[2] = brk ? 1.0 : 0.0;
+      if (!stop) {
+        // first pass coefficients of column t (w = z / eta)
+        double ab = 0.0;
+        if (t >= 1)
+          for (int c = 0; c < pb; ++c) ab += A_[c] * BB[c];
+        for (int c = 0; c < kc; ++c) S.bp[c] = BB[c] / eta;
+        for (int q = 0; q < t; ++q) S.hp[q] = BB[kc + q] / eta;
+        S.hp[t] = (mu_ - ab) / (eta * eta);
+        double cc2 = 0.0;
+        for (int c = 0; c < kc; ++c) cc2 += BB[c] * BB[c];
+        wn0_pending = sqrt(fmax(ze_ - cc2, 0.0)) / eta;
+        S.sc[3] = S.hp[t];
+      }
+    }
+    __syncthreads();
+    const double eta = S.sc[0];
+    const bool stop = S.sc[1] != 0.0;
+    brk = S.sc[2] != 0.0;
+    // coefficient vectors for sweep 2
+    for (int c = tid; c < pb; c += NT) {
+      S.a[c] = (t >= 1) ? S.red[3 + c] : 0.0;
+      S.bb[c] = stop ? 0.0 : S.red[3 + pb + c] / eta;
+    }
+    __syncthreads();
+    // ---- sweep 2: finish V_t, project the new vector into V_{t+1} ----------
+    {
+      const double htt = S.sc[3];
+      double* Vn = colV(p, t + 1);
+      for (int row = r0 + tid; row < r1; row += NT) {
+        double wv = Vt[row];
+        double ta = 0.0, tb = 0.0;
+        const double* q0 = Qb + row;
+        if (t >= 1 || !stop) {
+          for (int c = 0; c < pb; ++c) {
+            double qv = q0[(size_t)c * ld];
+            ta += qv * S.a[c];
+            tb += qv * S.bb[c];
+          }
+        }
+        double vt = wv;
+        if (t >= 1) {
+          vt = brk ? 0.0 : (wv - ta) / eta;
+          Vt[row] = vt;
+        }
+        if (!stop) Vn[row] = p.z[row] / eta - tb - vt * htt;
+      }
+    }
+    if (stop) {
+      j = t;
+      // CTA 0: y = R^-1 g (warp 0), y1 = (cr - B y2) / dk
+      if (blk == 0 && warp == 0) {
+        for (int q = lane; q < j; q += 32) S.y[kc + q] = S.gv[q];
+        __syncwarp();
+        for (int kk = j - 1; kk >= 0; --kk) {
+          double yk = S.y[kc + kk] / st->R[kk + kk * LDR];
+          __syncwarp();
+          for (int q = lane; q < kk; q += 32) S.y[kc + q] -= st->R[q + kk * LDR] * yk;
+          if (lane == 0) S.y[kc + kk] = yk;
+          __syncwarp();
+        }
+        for (int c = lane; c < kc; c += 32) {
+          double sacc = S.cr[c];
+          for (int q = 0; q < j; ++q) sacc -= st->B[c + q * LDB] * S.y[kc + q];
+          S.y[c] = sacc / S.dk[c];
+        }
+        __syncwarp();
+        for (int q = lane; q < kc + j; q += 32) st->y[q] = S.y[q];
+      }
+      if (blk == 0 && tid == 0) {
+        st->j = j;
+        st->brk = brk ? 1 : 0;
+        st->g[0] = hres;
+      }
+      CYCLE_SYNC();
+      break;
+    }
+    CYCLE_SYNC();
+  }
+
+  // ---- x update: x += U (dk y1) + V y2 ---------------------------------------
+  for (int q = tid; q < kc + j; q += NT) {
+    double yv = st->y[q];
+    S.y[q] = (q < kc) ? yv * S.dk[q] : yv;
+  }
+  __syncthreads();
+  for (int row = r0 + tid; row < r1; row += NT) {
+    double su = 0.0, sv = 0.0;
+    for (int c = 0; c < kc; ++c) su += colU(p, c)[row] * S.y[c];
+    for (int v = 0; v < j; ++v) sv += colV(p, v)[row] * S.y[kc + v];
+    p.x[row] = p.x[row] + (su + sv);
+  }
+  CYCLE_SYNC();
+
+  // ---- explicit residual + cross-Gram partials -------------------------------
+  double rr = 0.0;
+  for (int row = r0 + tid; row < r1; row += NT) {
+    double rv = __dsub_rn(__ldg(p.b + row), csr_row(p.rp, p.ci, p.av, p.x, row));
+    if (p.dg) rv = __ddiv_rn(rv, __ldg(p.dg + row));
+    p.r[row] = rv;
+    rr += rv * rv;
+  }
+  const int mm = kc + j;
+  if (defl) {
+    // staged columns: [U (kc) | C (kc) | V_0..V_{j-1}]
+    const int ncs = 2 * kc + j;
+    const int ne = mm * mm;
+    double gacc[(MMAX * MMAX + NT - 1) / NT];
+#pragma unroll
+    for (int q = 0; q < (MMAX * MMAX + NT - 1) / NT; ++q) gacc[q] = 0.0;
+    for (int t0 = r0; t0 < r1; t0 += 16) {
+      for (int e = tid; e < 16 * ncs; e += NT) {
+        int rrw = e % 16, c = e / 16;
+        int row = t0 + rrw;
+        const double* col = (c < kc) ? colU(p, c)
+                            : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc))
+                                           : colV(p, c - 2 * kc);
+        gtile[rrw][c] = row < r1 ? col[row] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < (MMAX * MMAX + NT - 1) / NT; ++q) {
+        int e = tid + q * NT;
+        if (e < ne) {
+          int a = e % mm, b = e / mm;
+          int ca = (a < kc) ? kc + a : 2 * kc + (a - kc);  // What col: C or V
+          int cb = (b < kc) ? b : 2 * kc + (b - kc);       // Vhat col: U or V
+          double sacc = 0.0;
+#pragma unroll
+          for (int rrw = 0; rrw < 16; ++rrw) sacc += gtile[rrw][ca] * gtile[rrw][cb];
+          gacc[q] += sacc;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < (MMAX * MMAX + NT - 1) / NT; ++q) {
+      int e = tid + q * NT;
+      if (e < ne) p.part[(size_t)(8 + e) * GRID_MAX + blk] = gacc[q];
+    }
+  }
+  {
+    double t_rr = block_sum(rr, S.bred);
+    if (tid == 0) p.part[blk] = t_rr;
+  }
+  CYCLE_SYNC();
+  if (defl) {
+    // distributed reduction of the cross-Gram: entry e handled by warp (e % (nblk*NW))
+    int gw = blk * NW + warp;
+    int ngw = nblk * NW;
+    for (int e = gw; e < mm * mm; e += ngw) {
+      const double* q = p.part + (size_t)(8 + e) * GRID_MAX;
+      double sacc = 0.0;
+      for (int b = lane; b < nblk; b += 32) sacc += q[b];
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+      if (lane == 0) {
+        int a = e % mm, b = e / mm;
+        double v = (b < kc) ? sacc * st->dk[b] : sacc;  // Vhat = [U diag(dk), V]
+        st->cross[a + b * LDX] = v;
+      }
+    }
+  }
+  if (blk == 0) {
+    reduce_partials(p.part, GRID_MAX, nblk, 0, 1, S.red);
+    if (tid == 0) {
+      double rnorm = sqrt(S.red[0]);
+      st->rnorm = rnorm;
+      st->converged = rnorm <= abs_tol ? 1 : 0;
+      p.checks[2 * st->nchecks] = st->g[0];
+      p.checks[2 * st->nchecks + 1] = rnorm;
+      st->nchecks += 1;
+      st->hist_len += j;
+      st->iters += j;
+      if (defl) st->defl_steps += j;
+      st->cycles += 1;
+      st->ran = 1;
+      // SURVEY 8(d) algorithmic bytes: per step B_spmv + 8N(2p+6), p = basis width
+      double N = (double)n;
+      double nnz = (double)(__ldg(p.rp + n));
+      double bsp = 12.0 * nnz + 4.0 * (N + 1) + 16.0 * N;
+      double acc = 0.0;
+      for (int q = 0; q < j; ++q) {
+        int pw = kc + q + 1;
+        acc += bsp + 8.0 * N * (2.0 * pw + 6.0);
+      }
+      st->step_bytes += acc;
+    }
+  }
+  (void)cycle_id;
+}
+
+// ---------------------------------------------------------------------------
+// the single-CTA dense kernel (programs)
+// ---------------------------------------------------------------------------
+__device__ void set_done(State* st, int cycle) {
+  st->done = 1;
+  flag_host(st, cycle, 1);
+}
+
+__global__ void __launch_bounds__(NT) k_dense(Ptrs p, int prog, int arg, int cycle_id) {
+  State* st = p.st;
+  extern __shared__ double dsm[];
+  __shared__ int s_iw[8 * skrd::LDD];
+  __shared__ int s_kept[KMAX];
+  skrd::Ctx c = skrd::ctx();
+  skrd::Arena ar = skrd::make_arena(dsm, s_iw, c.nw);
+  const int tid = threadIdx.x;
+  switch (prog) {
+    case P_INIT: {
+      reduce_partials(p.part, GRID_MAX, p.nblk, 0, 3, ar.red);
+      if (tid == 0) {
+        double bn = sqrt(ar.red[0]);
+        st->bnorm = bn;
+        if (bn == 0.0) {
+          st->zero_rhs = 1;
+          st->converged = 1;
+          st->rnorm = 0.0;
+          p.hist[0] = 0.0;
+          st->hist_len = 1;
+          set_done(st, -1);
+        } else {
+          double bp = sqrt(ar.red[1]);
+          st->bprec = bp;
+          st->abs_tol = st->tol * bp;
+          double rn = sqrt(ar.red[2]);
+          st->rnorm = rn;
+          p.hist[0] = rn;
+          st->hist_len = 1;
+          st->kc = 0;
+          st->ncol_a = st->k_in;
+          if (st->k_in > 0) st->iters += st->k_in;  // gcrodr.py:363
+          st->converged = rn <= st->abs_tol ? 1 : 0;
+          if (st->k_in == 0 && (st->converged || st->iters >= st->max_iter)) set_done(st, -1);
+        }
+      }
+      break;
+    }
+    case P_CHOL1: {
+      if (st->done) break;
+      int nc = arg == 0 ? st->ncol_a : st->ncol_b;
+      if (nc <= 0) break;
+      // gram -> T1 (coefU or coefC block), R1
+      double* T = arg == 0 ? st->coefU : st->coefC;
+      int r = skrd::cholqr_pass1(c, ar, st->gram, LDK, nc, T, LDC, st->R1, LDK);
+      if (tid == 0) {
+        st->r_tmp = r;
+        st->cm_mode = arg == 0 ? CM_U_ONLY : CM_C_ONLY;
+        st->cm_nin_u = arg == 0 ? nc : 0;
+        st->cm_nout_u = arg == 0 ? r : 0;
+        st->cm_nin_c = arg == 0 ? 0 : nc;
+        st->cm_nout_c = arg == 0 ? 0 : r;
+        if (r < nc) st->warn |= (arg == 0 ? skrd::W_RANK_DROP : skrd::W_REFRESH_RANK);
+        if (arg == 0)
+          st->ncol_a = r;
+        else
+          st->ncol_b = r;
+        st->ncol_orig = nc;  // original width for pass 2
+      }
+      break;
+    }
+    case P_CHOL2: {
+      if (st->done) break;
+      int r = arg == 0 ? st->ncol_a : st->ncol_b;
+      int korig = st->ncol_orig;
+      if (r <= 0) {
+        if (tid == 0) {
+          st->kc = 0;
+          st->ncol_a = 0;
+          st->ncol_b = 0;
+          st->cm_mode = CM_U_ONLY;
+          st->cm_nin_u = 0;
+          st->cm_nout_u = 0;
+          st->cm_nin_c = 0;
+          st->cm_nout_c = 0;
+          if (st->converged || st->iters >= st->max_iter) set_done(st, -1);
+        }
+        break;
+      }
+      double* T2 = arg == 0 ? st->coefU : st->coefC;
+      double* Rinv = ar.M4;
+      // pass 2 on the materialised X1 (its Gram reduced into st->gram)
+      int r2 = skrd::cholqr_pass2(c, ar, st->gram, LDK, r, st->R1, LDK, korig, T2, LDC, s_kept,
+                                  Rinv, skrd::LDD);
+      if (arg == 1 && r2 > 0) {
+        // U = Yo[:, kept] R'^-1 : coefU (ncol_a x r2), rows = Yo columns
+        int ry = st->ncol_a;
+        for (int e = tid; e < ry * r2; e += NT) {
+          int i = e % ry, q = e / ry;
+          double sacc = 0.0;
+          for (int t = 0; t <= q; ++t)
+            if (s_kept[t] == i) sacc += Rinv[t + q * skrd::LDD];
+          st->coefU[i + q * LDC] = sacc;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (r2 < korig) st->warn |= (arg == 0 ? skrd::W_RANK_DROP : skrd::W_REFRESH_RANK);
+        if (arg == 0) {
+          st->ncol_a = r2;
+          st->ncol_b = r2;
+          st->cm_mode = CM_U_ONLY;
+          st->cm_nin_u = r;
+          st->cm_nout_u = r2;
+          st->cm_nin_c = 0;
+          st->cm_nout_c = 0;
+          if (r2 == 0) {
+            st->kc = 0;
+            if (st->converged || st->iters >= st->max_iter) set_done(st, -1);
+          }
+        } else {
+          st->cm_mode = CM_REFRESH;
+          st->cm_nin_c = r;
+          st->cm_nout_c = r2;
+          st->cm_nin_u = st->ncol_a;
+          st->cm_nout_u = r2;
+          st->kc = r2;
+          if (r2 == 0) {
+            st->ncol_a = 0;
+            if (st->converged || st->iters >= st->max_iter) set_done(st, -1);
+          }
+        }
+      }
+      break;
+    }
+    case P_PROJ_FIN: {
+      if (st->done || st->kc == 0) break;
+      int kc = st->kc;
+      reduce_partials(p.part, GRID_MAX, p.nblk, 2 * kc, 1, ar.red);
+      if (tid == 0) {
+        double rn = sqrt(ar.red[0]);
+        st->rnorm = rn;
+        p.hist[st->hist_len] = rn;
+        st->hist_len += 1;
+        st->converged = rn <= st->abs_tol ? 1 : 0;
+        if (st->converged || st->iters >= st->max_iter) set_done(st, -1);
+      }
+      break;
+    }
+    case P_CYCLE: {
+      if (!st->ran) break;
+      int kc = st->kc, j = st->j;
+      int warn = 0;
+      int r;
+      if (st->k == 0) {
+        r = 0;  // k == 0: plain restarted GMRES, no recycle space (gcrodr.py:326-330)
+      } else if (kc == 0) {
+        r = skrd::recycle_first(c, ar, st->H, LDH, j, st->k, st->coefU, LDC, st->coefC, LDC, &warn);
+      } else {
+        r = skrd::recycle_next(c, ar, st->H, LDH, st->B, LDB, st->dk, kc, j, st->cross, LDX, st->k,
+                               st->coefU, LDC, st->coefC, LDC, &warn);
+      }
+      if (tid == 0) {
+        st->warn |= warn;
+        if (r < 0) st->status |= (1 << (-r));
+        st->kc_prev = kc;
+        if (r > 0) {
+          st->upd = 1;
+          st->k_new = r;
+          st->kc = r;
+        } else {
+          st->upd = 0;
+          st->k_new = kc;  // unchanged (None stays None)
+        }
+        bool done = st->converged || (st->brk && !st->converged) || st->iters >= st->max_iter;
+        if (done) {
+          set_done(st, cycle_id);
+        } else {
+          flag_host(st, cycle_id, 0);
+        }
+      }
+      break;
+    }
+    case P_FINAL: {
+      reduce_partials(p.part, GRID_MAX, p.nblk, 0, 1, ar.red);
+      if (tid == 0) {
+        st->true_rel = st->bnorm > 0.0 ? sqrt(ar.red[0]) / st->bnorm : 0.0;
+        if (st->kc == 0) st->fallback = 1;
+      }
+      break;
+    }
+  }
+}
+
+// single-CTA test entry points for the harmonic Ritz programs
+__global__ void __launch_bounds__(NT) k_dense_hr(const double* H, int ldh, int m, int k,
+                                                 const double* G, int ldg, const double* cross,
+                                                 int ldx, double* P, int ldp, int* out) {
+  extern __shared__ double dsm[];
+  __shared__ int s_iw[8 * skrd::LDD];
+  skrd::Ctx c = skrd::ctx();
+  skrd::Arena ar = skrd::make_arena(dsm, s_iw, c.nw);
+  int warn = 0;
+  int r;
+  if (H) {
+    r = skrd::hr_first(c, ar, H, ldh, m, k, &warn);
+  } else {
+    for (int e = threadIdx.x; e < (m + 1) * m; e += NT)
+      ar.G[(e % (m + 1)) + (e / (m + 1)) * skrd::LDD] = G[(e % (m + 1)) + (e / (m + 1)) * ldg];
+    __syncthreads();
+    r = skrd::hr_next(c, ar, m, cross, ldx, k, &warn);
+  }
+  int rows = m;
+  if (r > 0)
+    for (int e = threadIdx.x; e < rows * r; e += NT)
+      P[(e % rows) + (e / rows) * ldp] = ar.M2[(e % rows) + (e / rows) * skrd::LDD];
+  if (threadIdx.x == 0) {
+    out[0] = r;
+    out[1] = warn;
+  }
+}
+
+// standalone SpMV / residual kernels (K1)
+__global__ void __launch_bounds__(NT) k_spmv(int n, const int32_t* rp, const int32_t* ci,
+                                              const double* av, const double* dg, const double* x,
+                                              double* y) {
+  for (int row = blockIdx.x * NT + threadIdx.x; row < n; row += gridDim.x * NT) {
+    double v = csr_row(rp, ci, av, x, row);
+    if (dg) v = __ddiv_rn(v, __ldg(dg + row));
+    y[row] = v;
+  }
+}
+__global__ void __launch_bounds__(NT) k_resid(int n, const int32_t* rp, const int32_t* ci,
+                                               const double* av, const double* dg, const double* b,
+                                               const double* x, double* r) {
+  for (int row = blockIdx.x * NT + threadIdx.x; row < n; row += gridDim.x * NT) {
+    double v = __dsub_rn(__ldg(b + row), csr_row(rp, ci, av, x, row));
+    if (dg) v = __ddiv_rn(v, __ldg(dg + row));
+    r[row] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static size_t dense_smem_bytes() { return skrd::arena_doubles(NW) * sizeof(double); }
+
+struct DevInfo {
+  int sms = 0;
+  int cycle_blocks_per_sm = 0;
+  long long l2 = 0;
+  bool ok = false;
+};
+static DevInfo g_dev[16];
+static std::mutex g_mu;
+
+static int ensure_dev(DevInfo** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SKR_ERR_CUDA;
+  if (dev < 0 || dev >= 16) return SKR_ERR_UNSUPPORTED;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo& d = g_dev[dev];
+  if (!d.ok) {
+    if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    d.l2 = l2;
+    if (cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dense_smem_bytes()) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    if (cudaFuncSetAttribute(k_dense_hr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dense_smem_bytes()) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle, NT, 0) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    d.cycle_blocks_per_sm = nb;
+    const int combine_smem = 2 * LDC * KMAX * (int)sizeof(double);
+    cudaFuncSetAttribute(k_combine<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
+    cudaFuncSetAttribute(k_combine<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
+    cudaFuncSetAttribute(k_combine<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
+    cudaFuncSetAttribute(k_combine<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
+    d.ok = true;
+  }
+  *out = &d;
+  return SKR_OK;
+}
+
+// mapped host flags for the cycle look-ahead
+static int* g_flags_host = nullptr;
+static int* g_flags_dev = nullptr;
+static std::atomic<unsigned long long> g_slot_mask{0};
+
+static int acquire_slot(int** hptr, int** dptr) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_flags_host) {
+      if (cudaHostAlloc((void**)&g_flags_host, 64 * 2 * sizeof(int), cudaHostAllocMapped) !=
+          cudaSuccess)
+        return -1;
+      if (cudaHostGetDevicePointer((void**)&g_flags_dev, g_flags_host, 0) != cudaSuccess)
+        return -1;
+    }
+  }
+  for (int i = 0; i < 64; ++i) {
+    unsigned long long bit = 1ull << i;
+    unsigned long long old = g_slot_mask.fetch_or(bit);
+    if (!(old & bit)) {
+      *hptr = g_flags_host + 2 * i;
+      *dptr = g_flags_dev + 2 * i;
+      return i;
+    }
+  }
+  return -1;
+}
+static void release_slot(int i) {
+  if (i >= 0) g_slot_mask.fetch_and(~(1ull << i));
+}
+
+static int cfg_nblk(const DevInfo& d, int n) {
+  int maxb = std::min(GRID_MAX, d.sms * std::max(1, d.cycle_blocks_per_sm));
+  int want = (n + 255) / 256;  // at least 256 rows per CTA
+  return std::max(1, std::min(maxb, want));
+}
+
+static int launch_combine(int kt, Ptrs p, int nblk, int cycle_mode, cudaStream_t s) {
+  const int smem = 2 * LDC * KMAX * (int)sizeof(double);
+  if (kt <= 8)
+    k_combine<8><<<nblk, NT, smem, s>>>(p, cycle_mode);
+  else if (kt <= 16)
+    k_combine<16><<<nblk, NT, smem, s>>>(p, cycle_mode);
+  else if (kt <= 24)
+    k_combine<24><<<nblk, NT, smem, s>>>(p, cycle_mode);
+  else
+    k_combine<32><<<nblk, NT, smem, s>>>(p, cycle_mode);
+  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+}
+
+}  // namespace skr
+
+using namespace skr;
+
+extern "C" {
+
+int skr_version(void) { return 100; }
+
+const char* skr_status_string(int s) {
+  switch (s) {
+    case SKR_OK: return "ok";
+    case SKR_ERR_ARG: return "invalid argument";
+    case SKR_ERR_WORKSPACE: return "workspace too small";
+    case SKR_ERR_CUDA: return "CUDA error";
+    case SKR_ERR_TIMEOUT: return "timeout";
+    case SKR_ERR_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown";
+}
+
+int skr_device_info(int* sm_count, long long* l2_bytes) {
+  DevInfo* d;
+  int rc = ensure_dev(&d);
+  if (rc) return rc;
+  if (sm_count) *sm_count = d->sms;
+  if (l2_bytes) *l2_bytes = d->l2;
+  return SKR_OK;
+}
+
+int skr_spmv(const skr_csr* A, const double* x, double* y, int apply_prec, void* stream) {
+  if (!A || A->n < 0 || (A->n > 0 && (!x || !y || !A->row_ptr))) return SKR_ERR_ARG;
+  if (A->n == 0) return SKR_OK;
+  int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
+  k_spmv<<<grid, NT, 0, (cudaStream_t)stream>>>(A->n, A->row_ptr, A->col_idx, A->values,
+                                                 apply_prec ? A->diag : nullptr, x, y);
+  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+}
+
+int skr_residual(const skr_csr* A, const double* b, const double* x, double* r, int apply_prec,
+                 void* stream) {
+  if (!A || A->n < 0) return SKR_ERR_ARG;
+  if (A->n == 0) return SKR_OK;
+  int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
+  k_resid<<<grid, NT, 0, (cudaStream_t)stream>>>(A->n, A->row_ptr, A->col_idx, A->values,
+                                                  apply_prec ? A->diag : nullptr, b, x, r);
+  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+}
+
+size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter) {
+  if (n < 0 || m < 2 || k < 0 || k >= m || m + 1 > MMAX || k + 1 > KMAX || max_iter < 1) return 0;
+  return make_layout(n, m, k, max_iter).total;
+}
+
+int skr_gcrodr_recycle_view(void* ws, size_t ws_bytes, int32_t n, int32_t m, int32_t k, double** U,
+                            double** C, int32_t* k_out, int32_t* ld) {
+  if (!ws) return SKR_ERR_ARG;
+  Layout L = make_layout(n, m, k, 1);
+  (void)ws_bytes;
+  char* base = (char*)ws;
+  State* st = (State*)(base + L.state);
+  int kc = 0;
+  if (cudaMemcpy(&kc, &st->kc, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return SKR_ERR_CUDA;
+  double* basis = (double*)(base + L.basis);
+  if (U) *U = basis;
+  if (C) *C = basis + (size_t)(L.kcap + L.kcap - kc) * L.ld;
+  if (k_out) *k_out = kc;
+  if (ld) *ld = L.ld;
+  return SKR_OK;
+}
+
+int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double* x,
+                     const skr_config* cfg, const double* U_in, int32_t ldu, int32_t k_in,
+                     void* ws, size_t ws_bytes, skr_report* rep, double* hist, int32_t hist_cap,
+                     double* checks, int32_t checks_cap, void* stream_) {
+  if (!A || !b || !x || !cfg || !ws || !rep) return SKR_ERR_ARG;
+  const int n = A->n;
+  if (n <= 0 || cfg->m < 2 || cfg->k < 0 || cfg->k >= cfg->m || !(cfg->tol > 0) ||
+      cfg->max_iter < 1)
+    return SKR_ERR_ARG;
+  if (cfg->m + 1 > MMAX || cfg->k + 1 > KMAX) return SKR_ERR_UNSUPPORTED;
+  if (k_in < 0 || k_in > cfg->k + 1 || (k_in > 0 && (!U_in || ldu < n))) return SKR_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream_;
+  DevInfo* d;
+  int rc = ensure_dev(&d);
+  if (rc) return rc;
+  Layout L = make_layout(n, cfg->m, cfg->k, cfg->max_iter);
+  if (ws_bytes < L.total) return SKR_ERR_WORKSPACE;
+  char* base = (char*)ws;
+  Ptrs p;
+  p.st = (State*)(base + L.state);
+  p.rp = A->row_ptr;
+  p.ci = A->col_idx;
+  p.av = A->values;
+  p.dg = A->diag;
+  p.b = b;
+  p.x = x;
+  p.r = (double*)(base + L.r);
+  p.z = (double*)(base + L.z);
+  p.basis = (double*)(base + L.basis);
+  p.part = (double*)(base + L.part);
+  p.hist = (double*)(base + L.hist);
+  p.checks = (double*)(base + L.checks);
+  p.n = n;
+  p.ld = L.ld;
+  p.kcap = L.kcap;
+  const int nblk = cfg_nblk(*d, n);
+  p.nblk = nblk;
+  p.rpb = (int)align_up((size_t)((n + nblk - 1) / nblk), 32);
+  const int kt = L.kcap;
+  const int k_eff = cfg->k == 0 ? 0 : k_in;
+
+  int* hflag = nullptr;
+  int* dflag = nullptr;
+  int slot = acquire_slot(&hflag, &dflag);
+  if (slot < 0) return SKR_ERR_CUDA;
+  hflag[0] = -1;
+  hflag[1] = 0;
+
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, s);
+  k_setup<<<1, NT, 0, s>>>(p.st, n, L.ld, cfg->m, cfg->k, cfg->max_iter, cfg->tol,
+                           A->diag ? 1 : 0, nblk, p.rpb, k_eff, x0 ? 1 : 0, dflag);
+  if (k_eff > 0 && U_in != p.basis) {
+    cudaMemcpy2DAsync(p.basis, (size_t)L.ld * sizeof(double), U_in, (size_t)ldu * sizeof(double),
+                      (size_t)n * sizeof(double), k_eff, cudaMemcpyDeviceToDevice, s);
+  }
+  k_init<<<nblk, NT, 0, s>>>(p, x0);
+  const size_t dsm = dense_smem_bytes();
+  k_dense<<<1, NT, dsm, s>>>(p, P_INIT, 0, -1);
+  if (k_eff > 0) {
+    // orth(U_in): CholQR pass 1 + pass 2 with QRCP(R)
+    k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
+    k_reduce<<<8, NT, 0, s>>>(p, 0, 0);
+    k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 0, -1);
+    launch_combine(kt, p, nblk, 0, s);
+    k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
+    k_reduce<<<8, NT, 0, s>>>(p, 0, 0);
+    k_dense<<<1, NT, dsm, s>>>(p, P_CHOL2, 0, -1);
+    launch_combine(kt, p, nblk, 0, s);
+    // W = op(Yo) into the C block; QRCP(W) -> C, U
+    k_spmm<<<nblk, NT, 0, s>>>(p);
+    k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
+    k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
+    k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 1, -1);
+    launch_combine(kt, p, nblk, 0, s);
+    k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
+    k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
+    k_dense<<<1, NT, dsm, s>>>(p, P_CHOL2, 1, -1);
+    launch_combine(kt, p, nblk, 0, s);
+    // projection alpha = C^T r ; x += U alpha ; r -= C alpha
+    k_ctr<<<nblk, NT, 0, s>>>(p);
+    k_reduce<<<8, NT, 0, s>>>(p, 2, 0);
+    k_project<<<nblk, NT, 0, s>>>(p);
+    k_dense<<<1, NT, dsm, s>>>(p, P_PROJ_FIN, 0, -1);
+  }
+  if (cudaGetLastError() != cudaSuccess) {
+    release_slot(slot);
+    return SKR_ERR_CUDA;
+  }
+  // cycles with look-ahead
+  const int LOOK = 2;
+  int enq = 0, seen = 0;
+  int result = SKR_OK;
+  void* cargs[2];
+  int cyc = 0;
+  cargs[0] = &p;
+  cargs[1] = &cyc;
+  auto t_last = std::chrono::steady_clock::now();
+  while (true) {
+    volatile int* vf = hflag;
+    if (vf[1]) break;
+    while (enq < seen + LOOK) {
+      cyc = enq;
+      cudaError_t e = cudaLaunchCooperativeKernel((void*)k_cycle, dim3(nblk), dim3(NT), cargs, 0, s);
+      if (e != cudaSuccess) {
+        result = SKR_ERR_CUDA;
+        break;
+      }
+      k_dense<<<1, NT, dsm, s>>>(p, P_CYCLE, 0, enq);
+      launch_combine(kt, p, nblk, 1, s);
+      ++enq;
+    }
+    if (result) break;
+    // wait for cycle `seen` to be processed (or done)
+    while (true) {
+      if (vf[1]) break;
+      if (vf[0] >= seen) break;
+      cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) {
+        // stream drained: either done (flag) or stalled; re-check
+        if (vf[1] || vf[0] >= seen) break;
+        // nothing pending and no progress flag: the state says done
+        State hs;
+        cudaMemcpy(&hs.done, &p.st->done, sizeof(int), cudaMemcpyDeviceToHost);
+        if (hs.done) {
+          vf[1] = 1;
+          break;
+        }
+        if (vf[0] < seen) {
+          // the cycle ran without flagging: count it as processed
+          break;
+        }
+      } else if (q != cudaErrorNotReady) {
+        result = SKR_ERR_CUDA;
+        break;
+      }
+      auto now = std::chrono::steady_clock::now();
+      if (std::chrono::duration_cast<std::chrono::seconds>(now - t_last).count() > 120) {
+        result = SKR_ERR_TIMEOUT;
+        break;
+      }
+    }
+    if (result) break;
+    t_last = std::chrono::steady_clock::now();
+    if (vf[1]) break;
+    ++seen;
+  }
+  k_final_resid<<<nblk, NT, 0, s>>>(p);
+  k_dense<<<1, NT, dsm, s>>>(p, P_FINAL, 0, -1);
+  cudaEventRecord(ev1, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    result = SKR_ERR_CUDA;
+  release_slot(slot);
+  if (result) {
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return result;
+  }
+  State hs;
+  cudaMemcpy(&hs, p.st, offsetof(State, kept), cudaMemcpyDeviceToHost);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (hs.abort_flag) return SKR_ERR_TIMEOUT;
+  memset(rep, 0, sizeof(*rep));
+  rep->iterations = hs.iters;
+  rep->converged = hs.converged;
+  rep->k_out = hs.kc;
+  rep->hist_len = hs.hist_len;
+  rep->n_checks = hs.nchecks;
+  rep->deflated_steps = hs.defl_steps;
+  rep->warn_bits = hs.warn;
+  rep->status_bits = hs.status;
+  rep->zero_rhs = hs.zero_rhs;
+  rep->gmres_fallback = hs.kc == 0 ? 1 : 0;
+  rep->cycles = hs.cycles;
+  rep->true_relative_residual = hs.true_rel;
+  rep->rnorm = hs.rnorm;
+  rep->abs_tol = hs.abs_tol;
+  rep->bnorm = hs.bnorm;
+  rep->device_ms = ms;
+  rep->spmv_ortho_bytes = hs.step_bytes;
+  if (hist && hist_cap > 0)
+    cudaMemcpy(hist, p.hist, sizeof(double) * std::min(hist_cap, hs.hist_len),
+               cudaMemcpyDeviceToHost);
+  if (checks && checks_cap > 0)
+    cudaMemcpy(checks, p.checks, sizeof(double) * 2 * std::min(checks_cap, hs.nchecks),
+               cudaMemcpyDeviceToHost);
+  return SKR_OK;
+}
+
+int skr_dense_hr_first(const double* H, int32_t ldh, int32_t m, int32_t k, double* P, int32_t ldp,
+                       int32_t* ncols, void* stream) {
+  if (!H || !P || !ncols || m < 1 || m > skrd::DMAX || ldh < m + 1 || ldp < m) return SKR_ERR_ARG;
+  DevInfo* d;
+  int rc = ensure_dev(&d);
+  if (rc) return rc;
+  int* dout;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMallocAsync((void**)&dout, 2 * sizeof(int), s) != cudaSuccess) return SKR_ERR_CUDA;
+  k_dense_hr<<<1, NT, dense_smem_bytes(), s>>>(H, ldh, m, k, nullptr, 0, nullptr, 0, P, ldp, dout);
+  int hout[2] = {0, 0};
+  cudaMemcpyAsync(hout, dout, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(dout, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return SKR_ERR_CUDA;
+  *ncols = hout[0];
+  return SKR_OK;
+}
+
+int skr_dense_hr_next(const double* G, int32_t ldg, const double* cross, int32_t ldx, int32_t mm,
+                      int32_t k, double* P, int32_t ldp, int32_t* ncols, void* stream) {
+  if (!G || !cross || !P || !ncols || mm < 1 || mm + 1 > skrd::LDD || ldg < mm + 1 || ldx < mm ||
+      ldp < mm)
+    return SKR_ERR_ARG;
+  DevInfo* d;
+  int rc = ensure_dev(&d);
+  if (rc) return rc;
+  int* dout;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMallocAsync((void**)&dout, 2 * sizeof(int), s) != cudaSuccess) return SKR_ERR_CUDA;
+  k_dense_hr<<<1, NT, dense_smem_bytes(), s>>>(nullptr, 0, mm, k, G, ldg, cross, ldx, P, ldp,
+                                                dout);
+  int hout[2] = {0, 0};
+  cudaMemcpyAsync(hout, dout, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(dout, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return SKR_ERR_CUDA;
+  *ncols = hout[0];
+  return SKR_OK;
+}
+
+}  // extern "C"

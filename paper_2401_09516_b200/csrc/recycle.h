@@ -1,0 +1,391 @@
+// Recycle-space "programs" run by the single-CTA dense kernel (and, for unit
+// tests, on the host): harmonic-Ritz recycle updates and the tall-skinny QR
+// steps of the between-system refresh. Built on dense.h.
+//
+// Reference steps restated (kryrec/gcrodr.py):
+//   first cycle  _first_cycle_recycle           gcrodr.py:280-292
+//   later cycles recycle update in gcrodr_solve  gcrodr.py:444-460
+//   refresh      refresh_recycle                gcrodr.py:80-113 (via CholQR2 + QRCP(R))
+//
+// The tall (N-row) products are NOT done here: these programs emit small
+// coefficient matrices that the row-parallel combine kernel applies
+// (U_new = [U | V] coefU, C_new = [C | V] coefC), so the span algebra is
+// identical to the reference while every N-length pass stays one HBM sweep.
+#pragma once
+#include "dense.h"
+
+namespace skrd {
+
+struct Arena {
+  double* G;   // LDD x LDD
+  double* M1;  // LDD x LDD
+  double* M2;  // LDD x LDD
+  double* M3;  // LDD x LDD
+  double* M4;  // LDD x LDD
+  double* vec;    // 12 * LDD
+  double* xwork;  // nw * 3 * DMAX
+  double* red;    // 64
+  int* iw;        // 8 * LDD
+};
+
+SKR_HD size_t arena_doubles(int nw) {
+  return (size_t)5 * LDD * LDD + 12 * LDD + (size_t)nw * 3 * DMAX + 64;
+}
+SKR_HD size_t arena_ints() { return 8 * LDD; }
+
+SKR_HD Arena make_arena(double* d, int* iw, int nw) {
+  Arena a;
+  size_t M = (size_t)LDD * LDD;
+  a.G = d;
+  a.M1 = d + M;
+  a.M2 = d + 2 * M;
+  a.M3 = d + 3 * M;
+  a.M4 = d + 4 * M;
+  a.vec = d + 5 * M;
+  a.xwork = a.vec + 12 * LDD;
+  a.red = a.xwork + (size_t)nw * 3 * DMAX;
+  a.iw = iw;
+  return a;
+}
+
+// exact reference singularity test: sigma_max == 0 or sigma_min < 1e-14 sigma_max
+SKR_HD bool svd_singular(const Ctx& c, Arena& ar, const double* A, int lda, int n, double* work) {
+  copy_mat(c, A, lda, work, LDD, n, n);
+  bsync();
+  double* sv = ar.vec + 8 * LDD;
+  jacobi_svd(c, work, LDD, n, n, 0, 0, sv, ar.red);
+  double mx = 0.0, mn = INFINITY;
+  for (int i = 0; i < n; ++i) {
+    mx = sv[i] > mx ? sv[i] : mx;
+    mn = sv[i] < mn ? sv[i] : mn;
+  }
+  bsync();
+  return mx == 0.0 || mn < SING_RTOL * mx;
+}
+
+// harmonic_ritz_first_cycle (gcrodr.py:173-206). H: (m+1) x m raw Arnoldi
+// Hessenberg (only H[:m,:m] and H[m, m-1] are used). Result P_o (m x r1,
+// orthonormal) in ar.M2; returns r1 >= 1, or -status.
+SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, int k, int* warn) {
+  if (m <= 0 || m > DMAX) return -D_LINALG_ERROR;
+  int kk = k < m ? k : m;
+  int* piv = ar.iw;
+  double hsub = DA(H, ldh, m, m - 1);
+  for (int e = c.tid; e < m * m; e += c.nt) {
+    int i = e % m, j = e / m;
+    DA(ar.M2, LDD, i, j) = DA(H, ldh, j, i);  // Hs^T
+    DA(ar.M1, LDD, i, j) = DA(H, ldh, i, j);  // Hs
+  }
+  bsync();
+  double fn = fro_norm(c, ar.M1, LDD, m, m, ar.red);
+  int info = 0;
+  lu_factor(c, ar.M2, LDD, m, piv, &info);
+  bool singular = info != 0;
+  if (!singular) {
+    // [e_m | I]
+    for (int e = c.tid; e < m * (m + 1); e += c.nt) {
+      int i = e % m, j = e / m;
+      DA(ar.M3, LDD, i, j) = (j == 0) ? (i == m - 1 ? 1.0 : 0.0) : (i == j - 1 ? 1.0 : 0.0);
+    }
+    bsync();
+    lu_solve(c, ar.M2, LDD, m, piv, ar.M3, LDD, m + 1);
+    double gn = fro_norm(c, ar.M3 + LDD, LDD, m, m, ar.red);
+    if (!(fn * gn < KAPPA_CERT)) {
+      *warn |= W_JACOBI_SVD;
+      singular = svd_singular(c, ar, ar.M1, LDD, m, ar.M4);
+    }
+  }
+  if (singular) {
+    // reference: generalized problem (H^T H + h^2 e e^T, H^T) via QZ -- not ported
+    *warn |= W_SINGULAR_H;
+    return -D_UNSUPPORTED;
+  }
+  // modified = Hs + h^2 f e_m^T
+  double h2 = hsub * hsub;
+  for (int i = c.tid; i < m; i += c.nt) DA(ar.M1, LDD, i, m - 1) += h2 * DA(ar.M3, LDD, i, 0);
+  bsync();
+  double* wr = ar.vec;
+  double* wi = ar.vec + LDD;
+  if (eig_schur(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD) != 0) return -D_QR_NOCONV;
+  int ncols = select_basis(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, kk, m, ar.M4, LDD, ar.iw + LDD,
+                           ar.xwork, ar.red);
+  if (ncols < 0) return -D_LINALG_ERROR;
+  int* jp = ar.iw + 6 * LDD;
+  int r1 = qrcp(c, ar.M4, LDD, m, ncols, jp, ar.M2, LDD, RANK_RTOL, ar.vec + 2 * LDD,
+                ar.vec + 5 * LDD);
+  return r1;
+}
+
+// harmonic_ritz_subsequent (gcrodr.py:209-240). G in ar.G ((mm+1) x mm),
+// cross: mm x mm (leading block of What^T Vhat). P_o (mm x r1) in ar.M2.
+SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx, int k, int* warn) {
+  if (mm <= 0 || mm > DMAX) return -D_LINALG_ERROR;
+  int kk = k < mm ? k : mm;
+  int* piv = ar.iw;
+  gemm(c, true, ar.G, LDD, ar.G, LDD, ar.M1, LDD, mm, mm, mm + 1);   // lhs = G^T G
+  gemm(c, true, ar.G, LDD, cross, ldx, ar.M2, LDD, mm, mm, mm);      // rhs = G[:mm]^T cross
+  bsync();
+  double fn = fro_norm(c, ar.M2, LDD, mm, mm, ar.red);
+  copy_mat(c, ar.M2, LDD, ar.M4, LDD, mm, mm);  // keep rhs
+  bsync();
+  int info = 0;
+  lu_factor(c, ar.M2, LDD, mm, piv, &info);
+  bool singular = info != 0;
+  if (!singular) {
+    for (int e = c.tid; e < mm * mm; e += c.nt) {
+      int i = e % mm, j = e / mm;
+      DA(ar.M3, LDD, i, j) = (i == j) ? 1.0 : 0.0;
+    }
+    bsync();
+    lu_solve(c, ar.M2, LDD, mm, piv, ar.M3, LDD, mm);
+    double gn = fro_norm(c, ar.M3, LDD, mm, mm, ar.red);
+    if (!(fn * gn < KAPPA_CERT)) {
+      *warn |= W_JACOBI_SVD;
+      singular = svd_singular(c, ar, ar.M4, LDD, mm, ar.M3);
+    }
+  }
+  if (singular) {
+    *warn |= W_SINGULAR_CROSS;
+    // pinv(rhs) via Jacobi SVD: M4 <- U S, M3 <- V
+    double* sv = ar.vec + 8 * LDD;
+    jacobi_svd(c, ar.M4, LDD, mm, mm, ar.M3, LDD, sv, ar.red);
+    double mx = 0.0;
+    for (int i = 0; i < mm; ++i) mx = sv[i] > mx ? sv[i] : mx;
+    double cut = 1e-15 * mx;  // numpy pinv default rcond
+    // pinv = sum_i V(:,i) (a_i / s_i^2)^T over s_i > cut  -> M2
+    for (int e = c.tid; e < mm * mm; e += c.nt) {
+      int i = e % mm, j = e / mm;
+      double s = 0.0;
+      for (int q = 0; q < mm; ++q)
+        if (sv[q] > cut) s += DA(ar.M3, LDD, i, q) * DA(ar.M4, LDD, j, q) / (sv[q] * sv[q]);
+      DA(ar.M2, LDD, i, j) = s;
+    }
+    bsync();
+    gemm(c, false, ar.M2, LDD, ar.M1, LDD, ar.M4, LDD, mm, mm, mm);  // pinv @ lhs
+    bsync();
+    copy_mat(c, ar.M4, LDD, ar.M1, LDD, mm, mm);
+    bsync();
+  } else {
+    lu_solve(c, ar.M2, LDD, mm, piv, ar.M1, LDD, mm);  // rhs^-1 lhs
+  }
+  double* wr = ar.vec;
+  double* wi = ar.vec + LDD;
+  if (eig_schur(c, ar.M1, LDD, mm, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD) != 0) return -D_QR_NOCONV;
+  int ncols = select_basis(c, ar.M1, LDD, mm, ar.M3, LDD, wr, wi, kk, mm, ar.M4, LDD,
+                           ar.iw + LDD, ar.xwork, ar.red);
+  if (ncols < 0) return -D_LINALG_ERROR;
+  int* jp = ar.iw + 6 * LDD;
+  return qrcp(c, ar.M4, LDD, mm, ncols, jp, ar.M2, LDD, RANK_RTOL, ar.vec + 2 * LDD,
+              ar.vec + 5 * LDD);
+}
+
+// Common tail: GP = G P_o ((rows) x r1) -> QRCP -> Q, R, kept; Z = P_o[:,kept] R^-1.
+// Writes coefC (rows x r2) = Q and Zc (cols x r2) = Z. Returns r2.
+SKR_HD int gp_tail(const Ctx& c, Arena& ar, int rows, int cols, int r1, double* Zc, int ldz,
+                   double* Qc, int ldq) {
+  gemm(c, false, ar.G, LDD, ar.M2, LDD, ar.M1, LDD, rows, r1, cols);
+  bsync();
+  int* jp = ar.iw + 6 * LDD;
+  int r2 = qrcp(c, ar.M1, LDD, rows, r1, jp, ar.M3, LDD, RANK_RTOL, ar.vec + 2 * LDD,
+                ar.vec + 5 * LDD);
+  if (r2 <= 0) return 0;
+  inv_upper(c, ar.M1, LDD, r2, ar.M4, LDD);
+  for (int e = c.tid; e < cols * r2; e += c.nt) {
+    int i = e % cols, j = e / cols;
+    double s = 0.0;
+    for (int q = 0; q <= j; ++q) s += DA(ar.M2, LDD, i, jp[q]) * DA(ar.M4, LDD, q, j);
+    DA(Zc, ldz, i, j) = s;
+  }
+  for (int e = c.tid; e < rows * r2; e += c.nt) {
+    int i = e % rows, j = e / rows;
+    DA(Qc, ldq, i, j) = DA(ar.M3, LDD, i, j);
+  }
+  bsync();
+  return r2;
+}
+
+// First-cycle recycle pair (gcrodr.py:280-292). H: (j+1) x j.
+// U = V[:, :j] coefU (coefU: j x r), C = V[:, :j+1] coefC ((j+1) x r).
+// Returns r >= 1, 0 when the rank collapsed, or -status (U stays None).
+SKR_HD int recycle_first(const Ctx& c, Arena& ar, const double* H, int ldh, int j, int k,
+                         double* coefU, int ldu, double* coefC, int ldcc, int* warn) {
+  int kk = k < j ? k : j;
+  int r1 = hr_first(c, ar, H, ldh, j, kk, warn);
+  if (r1 <= 0) return r1 < 0 ? r1 : 0;
+  for (int e = c.tid; e < (j + 1) * j; e += c.nt) {
+    int i = e % (j + 1), q = e / (j + 1);
+    DA(ar.G, LDD, i, q) = DA(H, ldh, i, q);
+  }
+  bsync();
+  return gp_tail(c, ar, j + 1, j, r1, coefU, ldu, coefC, ldcc);
+}
+
+// Subsequent-cycle update (gcrodr.py:444-460). mm = kc + j. G built from dk,
+// B (kc x j) and H ((j+1) x j). coefU rows: [U cols 0..kc) (dk folded in:
+// Vhat = [U diag(dk), V]) | V_0..V_{j-1}]; coefC rows: [C cols | V_0..V_j].
+SKR_HD int recycle_next(const Ctx& c, Arena& ar, const double* H, int ldh, const double* B,
+                        int ldb, const double* dk, int kc, int j, const double* cross, int ldx,
+                        int k, double* coefU, int ldu, double* coefC, int ldcc, int* warn) {
+  int mm = kc + j;
+  if (mm + 1 > LDD) return -D_LINALG_ERROR;
+  for (int e = c.tid; e < (mm + 1) * mm; e += c.nt) {
+    int i = e % (mm + 1), q = e / (mm + 1);
+    double v = 0.0;
+    if (i < kc && q < kc)
+      v = (i == q) ? dk[i] : 0.0;
+    else if (i < kc)
+      v = DA(B, ldb, i, q - kc);
+    else if (q >= kc)
+      v = DA(H, ldh, i - kc, q - kc);
+    DA(ar.G, LDD, i, q) = v;
+  }
+  bsync();
+  int r1 = hr_next(c, ar, mm, cross, ldx, k, warn);
+  if (r1 <= 0) return r1 < 0 ? r1 : 0;
+  int r2 = gp_tail(c, ar, mm + 1, mm, r1, coefU, ldu, coefC, ldcc);
+  if (r2 <= 0) return 0;
+  for (int e = c.tid; e < kc * r2; e += c.nt) {
+    int i = e % kc, q = e / kc;
+    DA(coefU, ldu, i, q) *= dk[i];
+  }
+  bsync();
+  return r2;
+}
+
+// ---------------------------------------------------------------------------
+// CholQR building blocks for the refresh (orth(U) and QRCP(op U)).
+// Pass 1: diagonally-scaled pivoted Cholesky of the Gram matrix Gm (k x k).
+// Columns whose scaled Schur diagonal falls below drop_tol are numerically
+// dependent at Gram precision and dropped. Outputs T1 (k x r: X T1 has
+// orthonormal columns spanning X[:, perm[:r]]) and R1 (r x k, original column
+// order, X ~= (X T1) R1). Returns r.
+// ---------------------------------------------------------------------------
+SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int k, double* T1,
+                        int ldt, double* R1, int ldr) {
+  double* S = ar.M1;
+  double* R = ar.M2;
+  double* dsq = ar.vec;       // sqrt(diag)
+  int* perm = ar.iw;          // k
+  int* meta = ar.iw + LDD;    // [0] = rank, [1] = pivot
+  const double drop_tol = 1e-13;
+  for (int i = c.tid; i < k; i += c.nt) {
+    double d = DA(Gm, ldg, i, i);
+    dsq[i] = d > 0.0 ? sqrt(d) : 0.0;
+    perm[i] = i;
+  }
+  bsync();
+  for (int e = c.tid; e < k * k; e += c.nt) {
+    int i = e % k, j = e / k;
+    double den = dsq[i] * dsq[j];
+    DA(S, LDD, i, j) = den > 0.0 ? DA(Gm, ldg, i, j) / den : 0.0;
+    DA(R, LDD, i, j) = 0.0;
+  }
+  bsync();
+  int rank = k;
+  for (int i = 0; i < k; ++i) {
+    if (c.tid == 0) {
+      int p = i;
+      double best = DA(S, LDD, i, i);
+      for (int q = i + 1; q < k; ++q)
+        if (DA(S, LDD, q, q) > best) {
+          best = DA(S, LDD, q, q);
+          p = q;
+        }
+      meta[1] = p;
+      meta[0] = (best > drop_tol) ? 1 : 0;
+    }
+    bsync();
+    if (!meta[0]) {
+      rank = i;
+      break;
+    }
+    int p = meta[1];
+    if (p != i) {
+      // symmetric swap of rows/cols i,p of S, columns of R (rows < i), perm
+      for (int q = c.tid; q < k; q += c.nt) {
+        double t = DA(S, LDD, i, q);
+        DA(S, LDD, i, q) = DA(S, LDD, p, q);
+        DA(S, LDD, p, q) = t;
+      }
+      bsync();
+      for (int q = c.tid; q < k; q += c.nt) {
+        double t = DA(S, LDD, q, i);
+        DA(S, LDD, q, i) = DA(S, LDD, q, p);
+        DA(S, LDD, q, p) = t;
+        if (q < i) {
+          double u = DA(R, LDD, q, i);
+          DA(R, LDD, q, i) = DA(R, LDD, q, p);
+          DA(R, LDD, q, p) = u;
+        }
+      }
+      if (c.tid == 0) {
+        int t = perm[i];
+        perm[i] = perm[p];
+        perm[p] = t;
+      }
+      bsync();
+    }
+    double rii = sqrt(DA(S, LDD, i, i));
+    for (int q = i + c.tid; q < k; q += c.nt)
+      DA(R, LDD, i, q) = (q == i) ? rii : DA(S, LDD, i, q) / rii;
+    bsync();
+    int rem = k - i - 1;
+    for (int e = c.tid; e < rem * rem; e += c.nt) {
+      int a = i + 1 + e % rem, b = i + 1 + e / rem;
+      DA(S, LDD, a, b) -= DA(R, LDD, i, a) * DA(R, LDD, i, b);
+    }
+    bsync();
+  }
+  // unscale: R_true(:, q) = R(:, q) * dsq[perm[q]]
+  for (int e = c.tid; e < rank * k; e += c.nt) {
+    int i = e % rank, q = e / rank;
+    DA(R, LDD, i, q) *= dsq[perm[q]];
+  }
+  bsync();
+  if (rank > 0) inv_upper(c, R, LDD, rank, ar.M3, LDD);
+  for (int e = c.tid; e < k * rank; e += c.nt) {
+    int i = e % k, q = e / k;
+    DA(T1, ldt, i, q) = 0.0;
+  }
+  bsync();
+  for (int e = c.tid; e < rank * rank; e += c.nt) {
+    int i = e % rank, q = e / rank;
+    DA(T1, ldt, perm[i], q) = DA(ar.M3, LDD, i, q);
+  }
+  for (int e = c.tid; e < rank * k; e += c.nt) {
+    int i = e % rank, q = e / rank;
+    DA(R1, ldr, i, perm[q]) = DA(R, LDD, i, q);
+  }
+  bsync();
+  return rank;
+}
+
+// Pass 2 + rank decision: Gram G2 (r x r) of X1 = X T1, R1 (r x k) from pass 1.
+// R_tot = R2 R1 and QRCP(R_tot) gives the reference's QRCP(X) pivots / rank
+// (|R'_ii| >= 1e-12 |R'_00|). Outputs T2 (r x r2): X1 T2 = Q[:, :r2] of
+// QRCP(X); kept[0..r2) = pivots into X's columns; Rinv (r2 x r2) = R'^-1.
+// Returns r2 (0 = collapsed).
+SKR_HD int cholqr_pass2(const Ctx& c, Arena& ar, const double* G2, int ldg, int r, const double* R1,
+                        int ldr, int k, double* T2, int ldt, int* kept, double* Rinv, int ldri) {
+  if (r <= 0) return 0;
+  // pass-2 Cholesky (pivoted routine: G2 ~ I, so it keeps every column)
+  double* T2a = ar.G;  // r x r2a
+  double* R2 = ar.M4;  // r2a x r (original order)
+  int r2a = cholqr_pass1(c, ar, G2, ldg, r, T2a, LDD, R2, LDD);
+  if (r2a <= 0) return 0;
+  // R_tot = R2 R1 (r2a x k) -> M1
+  gemm(c, false, R2, LDD, R1, ldr, ar.M1, LDD, r2a, k, r);
+  bsync();
+  int* jp = ar.iw + 6 * LDD;
+  int r2 = qrcp(c, ar.M1, LDD, r2a, k, jp, ar.M3, LDD, RANK_RTOL, ar.vec + 2 * LDD,
+                ar.vec + 5 * LDD);
+  if (r2 <= 0) return 0;
+  // T2 = T2a Q'[:, :r2]  (r x r2)
+  gemm(c, false, T2a, LDD, ar.M3, LDD, T2, ldt, r, r2, r2a);
+  inv_upper(c, ar.M1, LDD, r2, Rinv, ldri);
+  for (int i = c.tid; i < r2; i += c.nt) kept[i] = jp[i];
+  bsync();
+  return r2;
+}
+
+}  // namespace skrd

@@ -1,0 +1,106 @@
+// Shared device helpers: CSR row kernel (bit-exact with scipy csr_matvec),
+// grid barrier with timeout for cooperative persistent kernels, block/warp
+// reductions over per-CTA partial sums.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/skr.h"
+
+namespace skr {
+
+constexpr int NT = 256;              // threads per CTA (streaming kernels)
+constexpr int NW = NT / 32;          // warps per CTA
+constexpr int KMAX = 32;             // max recycle columns incl. pair widening (k+1)
+constexpr int MMAX = 64;             // max Arnoldi columns (m + 1)
+constexpr int QMAX = (KMAX + MMAX + NW - 1) / NW;  // basis columns per warp in the dot phase
+constexpr int GRID_MAX = 1184;       // max persistent CTAs (148 SMs x 8)
+constexpr int PV_STEP = 2 * (KMAX + MMAX) + 8;      // reduction values per Arnoldi step
+constexpr int PV_MAX = MMAX * MMAX;  // largest reduction (cross-Gram mm x mm)
+constexpr unsigned long long BARRIER_TIMEOUT_NS = 8000000000ull;  // 8 s
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// y_i = sum_k a_ik x_k, sequential in column order from 0.0, separate multiply
+// and add (scipy sparsetools csr_matvec). x may be written by the
+// running kernel, so it is read through the coherent path.
+__device__ __forceinline__ double csr_row(const int32_t* __restrict__ rp,
+                                          const int32_t* __restrict__ ci,
+                                          const double* __restrict__ av, const double* x, int r) {
+  int s = __ldg(rp + r), e = __ldg(rp + r + 1);
+  double acc = 0.0;
+  for (int q = s; q < e; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(av + q), x[__ldg(ci + q)]));
+  return acc;
+}
+
+// Grid-wide barrier for a cooperatively launched kernel. Thread 0 of each CTA
+// arrives on a counter and spins (with backoff) on a generation word; the last
+// arriver resets the counter and bumps the generation. A spin longer than
+// BARRIER_TIMEOUT_NS sets *abort instead of hanging the GPU. Returns false
+// when the solve was aborted (uniform across the CTA).
+__device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, int* abort_flag,
+                                          unsigned nblk, int* s_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = gen;
+    unsigned g = *vgen;
+    __threadfence();
+    unsigned arrived = atomicAdd(count, 1u);
+    if (arrived == nblk - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      unsigned long long t0 = gtimer();
+      unsigned ns = 8;
+      while (*vgen == g) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+        if (gtimer() - t0 > BARRIER_TIMEOUT_NS) {
+          atomicExch(abort_flag, 1);
+          break;
+        }
+        if (*(volatile int*)abort_flag) break;
+      }
+    }
+    __threadfence();
+    *s_flag = *(volatile int*)abort_flag;
+  }
+  __syncthreads();
+  return *s_flag == 0;
+}
+
+// Sum over CTAs of partial values part[v * pstride + b], b < nblk, for
+// v in [v0, v0 + nv), into out[v - v0]. Deterministic: every CTA (and every
+// call) sums in the same order. Block-cooperative; ends with __syncthreads.
+__device__ __forceinline__ void reduce_partials(const double* part, int pstride, int nblk, int v0,
+                                                int nv, double* out) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v = v0 + warp; v < v0 + nv; v += NW) {
+    const double* p = part + (size_t)v * pstride;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += p[b];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (lane == 0) out[v - v0] = s;
+  }
+  __syncthreads();
+}
+
+// Block sum of one value per thread (result valid in every thread).
+__device__ __forceinline__ double block_sum(double v, double* s_red) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < NW; ++w) t += s_red[w];
+  return t;
+}
+
+}  // namespace skr

@@ -1,0 +1,250 @@
+"""Synthetic inputs for the five BASELINE.json configurations (host, numpy).
+
+These generators replace the reference's KL/SE-kernel samplers
+(``kryrec/problems.py:97-162``), whose coefficient laws differ from the
+benchmark configs. What is kept from the reference are its discretisation
+conventions, so the assembled systems read exactly like ``assemble_darcy`` /
+``assemble_helmholtz`` output:
+
+* h = 1/(n+1) per axis, unknowns ordered x-fastest (``problems.py:266-268``);
+* the h^2-scaled negative-diagonal stencil: off-diagonals +face, diagonal
+  -sum(faces) accumulated in the order x-1, x+1, y-1, y+1[, z-1, z+1]
+  (``problems.py:338-354``);
+* harmonic-mean face coefficients 2 a_p a_q / (a_p + a_q), and a boundary face
+  takes the cell's own coefficient (wall value zero) (``problems.py:329-354``);
+* b = -h^2 f for the flux-form problems (``problems.py:336``), and the
+  Helmholtz diagonal shift (k h)^2 on the -4 / +1 Laplacian
+  (``problems.py:258-277``, ``:380-383``), with b = +h^2 f.
+
+Gaussian random fields are sampled spectrally with an orthonormal DCT
+(Neumann cosine modes): coefficient (pi^2 |kappa|^2 + tau^2)^-1, i.e.
+covariance (-Laplacian + tau^2 I)^-2, constant mode removed (zero-mean field,
+so the {3, 12} thresholding splits roughly evenly), then scaled to unit mean
+pointwise variance. All choices are documented in DESIGN.md §Inputs.
+Per-system randomness is ``default_rng([base_seed, idx])`` as the reference's
+batch generator seeds per system (``problems.py:488``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+from functools import lru_cache
+
+import numpy as np
+import scipy.fft as _fft
+
+__all__ = [
+    "CONFIGS",
+    "ConfigSpec",
+    "grf",
+    "system_params",
+    "assemble",
+    "csr_pattern",
+]
+
+BASE_SEED = 240109516
+
+
+@dataclass(frozen=True)
+class ConfigSpec:
+    cid: int
+    name: str
+    kind: str  # darcy_binary | poisson_lognormal | helmholtz
+    dim: int
+    n: int  # interior points per axis
+    n_systems: int
+    tau: float
+    m: int
+    k: int
+    precond: str
+    tol: float = 1e-8
+    max_iter: int = 10000
+    scale: float = 1.0  # exponent scale for poisson_lognormal
+    bump_sigma: float = 0.05
+
+    @property
+    def N(self) -> int:
+        return self.n ** self.dim
+
+    def reduced(self, n: int | None = None, n_systems: int | None = None, **kw):
+        """Same construction on a smaller grid / batch (parity-test sizes)."""
+        upd = dict(kw)
+        if n is not None:
+            upd["n"] = n
+        if n_systems is not None:
+            upd["n_systems"] = n_systems
+        return replace(self, **upd)
+
+
+# BASELINE.json "configs" [0..4]. C2's max_iter is raised above the reference
+# default (indefinite Helmholtz stagnates for >10k iterations).
+CONFIGS = {
+    0: ConfigSpec(0, "darcy2d_64", "darcy_binary", 2, 64, 256, 3.0, 30, 10, "none"),
+    1: ConfigSpec(1, "poisson2d_256", "poisson_lognormal", 2, 256, 1024, 4.0, 40, 10,
+                  "jacobi", scale=0.5),
+    2: ConfigSpec(2, "helmholtz2d_256", "helmholtz", 2, 256, 1024, 3.0, 60, 20, "none",
+                  max_iter=50000),
+    3: ConfigSpec(3, "darcy3d_128", "darcy_binary", 3, 128, 512, 3.0, 40, 20, "jacobi"),
+    4: ConfigSpec(4, "darcy2d_1024", "darcy_binary", 2, 1024, 4096, 3.0, 40, 10, "jacobi"),
+}
+
+
+@lru_cache(maxsize=16)
+def _spectrum(shape: tuple, tau: float) -> tuple[np.ndarray, float]:
+    lam = np.zeros(shape)
+    for ax, n in enumerate(shape):
+        kk = (np.pi * np.arange(n)) ** 2
+        lam = lam + kk.reshape([-1 if a == ax else 1 for a in range(len(shape))])
+    coef = 1.0 / (lam + tau * tau)
+    coef.flat[0] = 0.0  # zero-mean field (no constant mode), as in FNO-style Darcy data
+    norm = float(np.sqrt(np.sum(coef * coef) / coef.size))
+    return coef, norm
+
+
+def grf(shape: tuple, tau: float, rng: np.random.Generator) -> np.ndarray:
+    """Unit-mean-variance GRF with covariance (-Laplacian + tau^2)^-2 (DCT)."""
+    coef, norm = _spectrum(tuple(shape), float(tau))
+    xi = rng.standard_normal(shape)
+    g = _fft.idctn(xi * coef, type=2, norm="ortho", workers=-1)
+    return g / norm
+
+
+def _rng(spec: ConfigSpec, idx: int, stream: int = 0) -> np.random.Generator:
+    return np.random.default_rng([BASE_SEED, spec.cid, stream, int(idx)])
+
+
+def system_params(spec: ConfigSpec, idx: int) -> dict:
+    """The generative fields of system ``idx`` plus its sort parameter vector."""
+    shape = (spec.n,) * spec.dim
+    rng = _rng(spec, idx)
+    if spec.kind == "darcy_binary":
+        g = grf(shape, spec.tau, rng)
+        a = np.where(g > 0.0, 12.0, 3.0)
+        return {"a": a, "params": a.ravel()}
+    if spec.kind == "poisson_lognormal":
+        g = grf(shape, spec.tau, rng)
+        a = np.exp(spec.scale * g)
+        return {"a": a, "params": a.ravel()}
+    if spec.kind == "helmholtz":
+        k0 = float(rng.uniform(10.0, 20.0))
+        g = grf(shape, spec.tau, rng)
+        kf = k0 * (1.0 + 0.3 * np.tanh(g))
+        center = rng.uniform(0.2, 0.8, size=spec.dim)
+        return {"kfield": kf, "k0": k0, "g": g, "center": center,
+                "params": np.concatenate([[k0], g.ravel()])}
+    raise ValueError(f"unknown config kind {spec.kind!r}")
+
+
+@lru_cache(maxsize=8)
+def csr_pattern(dim: int, n: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Row pointers, column indices (int64) and a per-entry slot code.
+
+    Slot codes: 0 = diagonal, 1+2*ax = neighbour at -1 along axis ax,
+    2+2*ax = neighbour at +1 along axis ax. Columns are strictly increasing per
+    row, as ``CsrMatrix`` requires (``sparse.py:52-55``).
+    """
+    N = n ** dim
+    idx = np.arange(N).reshape((n,) * dim)  # C-order: last axis = x fastest
+    # axis order for the stencil: x (last array axis), y, z
+    entries = []  # (mask over cells, column offset, slot)
+    for ax in range(dim):
+        arr_ax = dim - 1 - ax
+        stride = n ** ax
+        coord = np.indices((n,) * dim)[arr_ax]
+        entries.append((coord > 0, -stride, 1 + 2 * ax))
+        entries.append((coord < n - 1, +stride, 2 + 2 * ax))
+    entries.append((np.ones((n,) * dim, dtype=bool), 0, 0))
+    # sort entries by column offset so columns increase within a row
+    entries.sort(key=lambda e: e[1])
+    counts = np.zeros(N, dtype=np.int64)
+    for mask, _, _ in entries:
+        counts += mask.ravel()
+    row_ptr = np.zeros(N + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    nnz = int(row_ptr[-1])
+    col = np.empty(nnz, dtype=np.int64)
+    slot = np.empty(nnz, dtype=np.int8)
+    fill = row_ptr[:-1].copy()
+    flat_idx = idx.ravel()
+    for mask, off, sl in entries:
+        rows = flat_idx[mask.ravel()]
+        pos = fill[rows]
+        col[pos] = rows + off
+        slot[pos] = sl
+        fill[rows] += 1
+    return row_ptr, col, slot
+
+
+def _faces_flux(a: np.ndarray):
+    """Per-cell face coefficients for -div(a grad u) (harmonic means)."""
+    dim = a.ndim
+    faces = []  # list over (ax, side) of arrays shaped like a
+    for ax in range(dim):
+        arr_ax = dim - 1 - ax
+        lo = np.empty_like(a)
+        hi = np.empty_like(a)
+        sl_lo = [slice(None)] * dim
+        sl_hi = [slice(None)] * dim
+        sl_lo[arr_ax] = slice(1, None)
+        sl_hi[arr_ax] = slice(None, -1)
+        ap, aq = a[tuple(sl_lo)], a[tuple(sl_hi)]
+        hm = 2.0 * ap * aq / (ap + aq)
+        # lower neighbour face of cell p (p has a lower neighbour) = hm
+        lo[tuple(sl_lo)] = hm
+        first = [slice(None)] * dim
+        first[arr_ax] = 0
+        lo[tuple(first)] = a[tuple(first)]  # wall face uses the cell value
+        hi[tuple(sl_hi)] = hm
+        last = [slice(None)] * dim
+        last[arr_ax] = -1
+        hi[tuple(last)] = a[tuple(last)]
+        faces.append((lo, hi))
+    return faces
+
+
+def assemble(spec: ConfigSpec, idx: int, fields: dict | None = None):
+    """Assemble system ``idx``: returns (row_ptr, col_idx, values, b, params).
+
+    Arrays are float64 / int64 numpy, ready for ``CsrMatrix``.
+    """
+    fields = fields if fields is not None else system_params(spec, idx)
+    dim, n = spec.dim, spec.n
+    N = n ** dim
+    h = 1.0 / (n + 1)
+    row_ptr, col, slot = csr_pattern(dim, n)
+    vals = np.empty(col.shape[0], dtype=np.float64)
+    rows = np.repeat(np.arange(N), np.diff(row_ptr))
+    if spec.kind in ("darcy_binary", "poisson_lognormal"):
+        faces = _faces_flux(fields["a"])
+        diag = np.zeros(N)
+        for ax in range(dim):
+            lo, hi = faces[ax]
+            lo, hi = lo.ravel(), hi.ravel()
+            diag = diag - lo  # x-1 then x+1 (reference order), then y, z
+            diag = diag - hi
+            m_lo = slot == 1 + 2 * ax
+            m_hi = slot == 2 + 2 * ax
+            vals[m_lo] = lo[rows[m_lo]]
+            vals[m_hi] = hi[rows[m_hi]]
+        vals[slot == 0] = diag
+        if spec.kind == "darcy_binary":
+            f = np.ones(N)
+        else:
+            f = np.random.default_rng([BASE_SEED, spec.cid, 7, 0]).standard_normal(N)
+        b = -(h * h) * f
+    elif spec.kind == "helmholtz":
+        shift = (fields["kfield"].ravel() * h) ** 2
+        vals[slot != 0] = 1.0
+        vals[slot == 0] = -2.0 * dim + shift
+        coords = [(np.arange(1, n + 1) * h)] * dim
+        grids = np.meshgrid(*coords, indexing="ij")  # arr axes (z, y, x)
+        c = fields["center"]
+        r2 = np.zeros((n,) * dim)
+        for arr_ax in range(dim):
+            ax = dim - 1 - arr_ax
+            r2 = r2 + (grids[arr_ax] - c[ax]) ** 2
+        f = np.exp(-r2 / (2.0 * spec.bump_sigma ** 2)).ravel()
+        b = (h * h) * f
+    else:
+        raise ValueError(spec.kind)
+    return row_ptr, col, vals, b, fields["params"]

@@ -1,0 +1,151 @@
+"""The SKR chain: solve a sorted sequence of systems carrying the recycle space.
+
+Restates the driving loop of the reference (kryrec/harness.py:233-260:
+``rep, recycle = gcrodr_solve(A, b, M, cfg, recycle_in=recycle)`` over the
+sorted order) for the device engine, with three B200-first changes:
+
+* the recycle pair never leaves the GPU -- system i+1's refresh reads U from
+  the workspace block system i left it in (no copies, no host round trip);
+* the next system's CSR / right-hand side is uploaded on a side stream while
+  the current one solves (double buffering), from pinned host memory when the
+  caller provides it;
+* multi-GPU: the sorted order splits into contiguous chunks, one independent
+  chain per rank (the paper's parallel SKR); there is no
+  collective on the solve path.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .gcrodr import engine_for
+from .gmres import SolverConfig
+from .sparse import DeviceCsr
+
+__all__ = ["SequenceResult", "solve_sequence", "chunk_positions"]
+
+
+@dataclass
+class SequenceResult:
+    order: list
+    iterations: list = field(default_factory=list)
+    converged: list = field(default_factory=list)
+    true_rel: list = field(default_factory=list)
+    device_ms: list = field(default_factory=list)
+    k_out: list = field(default_factory=list)
+    warn_bits: list = field(default_factory=list)
+    spmv_ortho_bytes: float = 0.0
+    x: list = field(default_factory=list)
+    wall_s: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+def chunk_positions(n: int, world: int, rank: int) -> range:
+    """Contiguous positions of the sorted order owned by ``rank``."""
+    per = -(-n // world)
+    lo = min(n, rank * per)
+    return range(lo, min(n, lo + per))
+
+
+def _nbytes(t) -> int:
+    return int(t.numel() * t.element_size())
+
+
+def _upload(sysobj, jacobi: bool, stream):
+    """Host system -> (DeviceCsr, b_dev, bytes). Accepts (A, b) pairs where the
+    arrays are numpy or (ideally pinned) torch CPU tensors, or a DeviceCsr."""
+    import torch
+
+    A, b = sysobj
+    if isinstance(A, DeviceCsr):
+        bt = b if isinstance(b, torch.Tensor) and b.is_cuda else torch.as_tensor(b).to("cuda")
+        return A, bt, 0
+    with torch.cuda.stream(stream):
+        dA = DeviceCsr.from_host(A, jacobi=False, non_blocking=True)
+        if isinstance(b, torch.Tensor):
+            bt = b.to("cuda", dtype=torch.float64, non_blocking=True)
+        else:
+            bt = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to("cuda")
+        nb = _nbytes(dA.row_ptr) + _nbytes(dA.col_idx) + _nbytes(dA.values) + _nbytes(bt)
+        if jacobi:
+            from .sparse import _device_diagonal
+
+            dA = dA.with_diag(_device_diagonal(dA.n, dA.row_ptr, dA.col_idx, dA.values))
+    return dA, bt, nb
+
+
+def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[int],
+                   cfg: SolverConfig, precond: str = "none", *, positions: Sequence[int] = None,
+                   keep_x: str = "host", stream=None, recycle_first=None,
+                   want_history: bool = False) -> SequenceResult:
+    """Solve ``systems[order[p]]`` for p in ``positions`` (default: all) as one
+    recycling chain. ``systems`` is a sequence of (A, b) or a callable idx ->
+    (A, b) (lazy generation for large configs). ``keep_x``: "host" (x copied
+    back per system), "device" (kept as CUDA tensors) or "none"."""
+    import torch
+
+    _lib.require_cuda()
+    if precond not in ("none", "jacobi"):
+        raise NotImplementedError(f"preconditioner {precond!r} is not on the device path")
+    jacobi = precond == "jacobi"
+    positions = list(range(len(order))) if positions is None else list(positions)
+    get = systems if callable(systems) else (lambda i: systems[i])
+    res = SequenceResult(order=[int(order[p]) for p in positions])
+    if not positions:
+        return res
+    main = stream if stream is not None else torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    t0 = time.perf_counter()
+    # first upload
+    nxt = _upload(get(res.order[0]), jacobi, side)
+    ev = torch.cuda.Event()
+    ev.record(side)
+    eng = None
+    k_prev = 0
+    U_prev_ptr, ld_prev = None, 0
+    if recycle_first is not None and recycle_first.k > 0:
+        from .gcrodr import _colmajor_device
+
+        Ud, ld_prev = _colmajor_device(recycle_first.U, recycle_first.U.shape[0])
+        U_prev_ptr, k_prev = Ud, int(Ud.shape[1])
+    for i, idx in enumerate(res.order):
+        main.wait_event(ev)
+        dA, bt, nb = nxt
+        res.h2d_bytes += nb
+        if eng is None:
+            eng = engine_for(dA.n, cfg)
+        # prefetch the next system while this one solves
+        if i + 1 < len(res.order):
+            nxt = _upload(get(res.order[i + 1]), jacobi, side)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        x = torch.empty(dA.n, dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(main):
+            rep = eng.solve(dA, bt, x, None, U_prev_ptr, ld_prev, k_prev, stream=main,
+                            want_history=want_history)
+        res.iterations.append(int(rep.iterations))
+        res.converged.append(bool(rep.converged))
+        res.true_rel.append(float(rep.true_relative_residual))
+        res.device_ms.append(float(rep.device_ms))
+        res.k_out.append(int(rep.k_out))
+        res.warn_bits.append(int(rep.warn_bits))
+        res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
+        if keep_x == "host":
+            res.x.append(x.cpu().numpy())
+            res.d2h_bytes += _nbytes(x)
+        elif keep_x == "device":
+            res.x.append(x)
+        # chain: the next refresh reads U where this solve left it
+        if cfg.k > 0 and not rep.zero_rhs:
+            U, C, k, ld = eng.recycle_views()
+            U_prev_ptr = U.data_ptr() if k else None
+            ld_prev, k_prev = ld, k
+    torch.cuda.synchronize()
+    res.wall_s = time.perf_counter() - t0
+    return res

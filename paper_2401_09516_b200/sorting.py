@@ -1,0 +1,143 @@
+"""Similarity ordering of a system batch on the GPU (kryrec/sorting.py).
+
+``greedy_sort`` keeps the reference's signature and result (sorting.py:72-80):
+start at index 0, repeatedly append the unvisited system nearest (Frobenius)
+to the previous pick, ties to the smallest index. The distance matrix and
+the chain run in libskr.so; see csrc/sort.cu for the exact / certified
+arithmetic that makes the permutation bit-identical to the reference.
+``sharded_greedy_sort`` splits the distance rows across ranks and gathers
+them with torch.distributed (NCCL on the GPU box).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["ParameterMatrix", "frobenius_distance", "greedy_sort", "greedy_sort_device",
+           "sharded_greedy_sort", "row_shard"]
+
+
+@dataclass(frozen=True)
+class ParameterMatrix:
+    """Generative parameters of one system (sorting.py:16-33)."""
+
+    values: np.ndarray
+    problem_id: int = 0
+
+    def __post_init__(self):
+        v = np.atleast_2d(np.asarray(self.values, dtype=np.float64))
+        if not np.all(np.isfinite(v)):
+            raise ValueError("parameter entries must be finite")
+        v = v.copy()
+        v.flags.writeable = False
+        object.__setattr__(self, "values", v)
+
+    @property
+    def flat(self) -> np.ndarray:
+        return self.values.ravel()
+
+
+def frobenius_distance(P: ParameterMatrix, Q: ParameterMatrix) -> float:
+    if P.values.shape != Q.values.shape:
+        raise ValueError(f"parameter shape mismatch: {P.values.shape} vs {Q.values.shape}")
+    return float(np.linalg.norm(P.values - Q.values, "fro"))
+
+
+def _stacked(params: Sequence) -> np.ndarray:
+    if not params:
+        raise ValueError("empty parameter batch")
+    vals = [p.values if isinstance(p, ParameterMatrix) else
+            np.atleast_2d(np.asarray(getattr(p, "values", p), dtype=np.float64))
+            for p in params]
+    shape = vals[0].shape
+    for v in vals[1:]:
+        if v.shape != shape:
+            raise ValueError("inconsistent parameter shapes in batch")
+    return np.stack([v.ravel() for v in vals])
+
+
+class _SortWorkspace:
+    cache: dict = {}
+
+    @classmethod
+    def get(cls, n_sys, P):
+        import torch
+
+        L = _lib.load()
+        need = int(L.skr_sort_workspace_bytes(int(n_sys), int(P)))
+        dev = torch.cuda.current_device()
+        ws = cls.cache.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+            cls.cache[dev] = ws
+        return ws, need
+
+
+def greedy_sort_device(flat_dev, stream=None) -> list[int]:
+    """Greedy order of the rows of a (n_sys, P) float64 CUDA tensor."""
+    L = _lib.load()
+    n_sys, P = flat_dev.shape
+    flat_dev = flat_dev.contiguous()
+    ws, need = _SortWorkspace.get(n_sys, P)
+    order = np.zeros(n_sys, dtype=np.int32)
+    _lib.check(L.skr_greedy_sort(flat_dev.data_ptr(), int(n_sys), int(P), order.ctypes.data,
+                                 ws.data_ptr(), need, _lib.stream_handle(stream)),
+               "skr_greedy_sort")
+    return [int(i) for i in order]
+
+
+def greedy_sort(params: Sequence[ParameterMatrix]) -> list[int]:
+    """Order the batch so consecutive parameter matrices are close (sorting.py:72-80)."""
+    import torch
+
+    flat = _stacked(params)
+    _lib.require_cuda()
+    return greedy_sort_device(torch.from_numpy(flat).to("cuda"))
+
+
+def row_shard(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row block [r0, r1) of rank ``rank`` out of ``world``."""
+    per = -(-n // world)
+    r0 = min(n, rank * per)
+    return r0, min(n, r0 + per)
+
+
+def sharded_greedy_sort(flat_dev, group=None, stream=None) -> list[int]:
+    """Multi-GPU greedy sort: D2 rows sharded by rank, NCCL all_gather, then the
+    (deterministic, replicated) chain on every rank. Every rank holds all params."""
+    import torch
+    import torch.distributed as dist
+
+    L = _lib.load()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n_sys, P = flat_dev.shape
+    flat_dev = flat_dev.contiguous()
+    ws, need = _SortWorkspace.get(n_sys, P)
+    sh = _lib.stream_handle(stream)
+    v = np.zeros(2)
+    isb = ctypes.c_int32()
+    _lib.check(L.skr_sort_binary_check(flat_dev.data_ptr(), n_sys, P, v.ctypes.data,
+                                       ctypes.byref(isb), ws.data_ptr(), need, sh), "binary_check")
+    per = -(-n_sys // world)
+    D2 = torch.zeros((per * world, n_sys), dtype=torch.float64, device="cuda")
+    r0, r1 = row_shard(n_sys, world, rank)
+    local = D2[rank * per: rank * per + per]
+    if r1 > r0:
+        _lib.check(L.skr_sort_dist2(flat_dev.data_ptr(), n_sys, P, r0, r1, isb.value,
+                                    float(v[0]), float(v[1]), local.data_ptr(), ws.data_ptr(),
+                                    need, sh), "dist2")
+    chunks = list(D2.split(per))
+    dist.all_gather(chunks, local.clone(), group=group)
+    D2 = torch.cat(chunks)[:n_sys].contiguous()
+    order = torch.zeros(n_sys, dtype=torch.int32, device="cuda")
+    ncert = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(L.skr_sort_chain(D2.data_ptr(), flat_dev.data_ptr(), n_sys, P, isb.value,
+                                order.data_ptr(), ncert.data_ptr(), sh), "chain")
+    return [int(i) for i in order.cpu()]

@@ -79,6 +79,10 @@ typedef struct skr_report {
   double bnorm;
   double device_ms;       /* device time of the solve (CUDA events) */
   double spmv_ortho_bytes;/* algorithmic bytes of the Arnoldi steps */
+  double cycle_kernel_ms; /* summed CUDA-event time of the Arnoldi-cycle kernel launches */
+  double dense_kernel_ms; /* summed time of the per-cycle recycle-update (dense) launches */
+  int32_t launches;       /* kernels this solve launched (incl. speculative no-op cycles) */
+  int32_t arnoldi_steps;  /* Arnoldi steps executed (SpMV + ortho), incl. the GMRES cycles */
 } skr_report;
 
 enum skr_warn {

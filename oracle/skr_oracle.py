@@ -59,6 +59,39 @@ def greedy_order(flat: np.ndarray) -> list[int]:
     return chain
 
 
+def greedy_order_prefix(flat: np.ndarray, npos: int) -> list[int]:
+    """The first ``npos`` positions of greedy_order (the chain is sequential, so
+    a prefix costs npos passes instead of n); same arithmetic."""
+    flat = np.asarray(flat, dtype=np.float64)
+    n = flat.shape[0]
+    visited = np.zeros(n, dtype=bool)
+    visited[0] = True
+    chain = [0]
+    while len(chain) < min(npos, n):
+        cand = np.flatnonzero(~visited)
+        d = np.linalg.norm(flat[cand] - flat[chain[-1]], axis=1)
+        nxt = int(cand[int(np.argmin(d))])
+        visited[nxt] = True
+        chain.append(nxt)
+    return chain
+
+
+def greedy_order_from_d2(D2: np.ndarray) -> list[int]:
+    """Greedy chain from a precomputed squared-distance matrix (sqrt, first
+    minimum) -- checker for the sharded-gather plumbing."""
+    D2 = np.asarray(D2, dtype=np.float64)
+    n = D2.shape[0]
+    visited = np.zeros(n, dtype=bool)
+    visited[0] = True
+    chain = [0]
+    for _ in range(n - 1):
+        cand = np.flatnonzero(~visited)
+        nxt = int(cand[int(np.argmin(np.sqrt(D2[chain[-1], cand])))])
+        visited[nxt] = True
+        chain.append(nxt)
+    return chain
+
+
 def pairwise_sum(a: np.ndarray) -> float:
     """numpy's float64 pairwise summation (blocks of 128, 8 accumulators).
 

@@ -24,7 +24,7 @@ from .precond import (
     ZeroPivotError,
     build_preconditioner,
 )
-from .sequence import SequenceResult, chunk_positions, solve_sequence
+from .sequence import ChainState, SequenceResult, chunk_positions, solve_sequence
 from .sorting import (
     ParameterMatrix,
     frobenius_distance,
@@ -37,7 +37,7 @@ from .sparse import CsrMatrix, DeviceCsr, axpy, dot, eye, norm2, spmv
 __version__ = "0.1.0"
 
 __all__ = [
-    "CsrMatrix", "DeviceCsr", "GcroDrEngine", "IdentityPreconditioner", "JacobiPreconditioner",
+    "ChainState", "CsrMatrix", "DeviceCsr", "GcroDrEngine", "IdentityPreconditioner", "JacobiPreconditioner",
     "ParameterMatrix", "Preconditioner", "RecycleSpace", "SequenceResult", "SolveReport",
     "SolverConfig", "ZeroPivotError", "axpy", "build_preconditioner", "chunk_positions", "dot",
     "eye", "frobenius_distance", "gcrodr_solve", "gmres_solve", "greedy_sort",

@@ -44,7 +44,9 @@ class SkrReport(ctypes.Structure):
                 ("gmres_fallback", c_int32), ("cycles", c_int32), ("reserved", c_int32),
                 ("true_relative_residual", c_double), ("rnorm", c_double),
                 ("abs_tol", c_double), ("bnorm", c_double), ("device_ms", c_double),
-                ("spmv_ortho_bytes", c_double)]
+                ("spmv_ortho_bytes", c_double), ("cycle_kernel_ms", c_double),
+                ("dense_kernel_ms", c_double), ("launches", c_int32),
+                ("arnoldi_steps", c_int32)]
 
 
 WARN_SINGULAR_H = 1

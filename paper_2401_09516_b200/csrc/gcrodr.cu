@@ -26,6 +26,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <vector>
 
 #include "recycle.h"
 #include "skr_device.cuh"
@@ -70,6 +71,7 @@ struct State {
   unsigned bar_count, bar_gen;
   int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
+  int steps, pad2;    // Arnoldi steps executed
   int kept[KMAX];
   // per-cycle small data
   double H[LDH * MMAX];
@@ -879,6 +881,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
       st->nchecks += 1;
       st->hist_len += j;
       st->iters += j;
+      st->steps += j;
       if (defl) st->defl_steps += j;
       st->cycles += 1;
       st->ran = 1;
@@ -1215,6 +1218,20 @@ static void release_slot(int i) {
   if (i >= 0) g_slot_mask.fetch_and(~(1ull << i));
 }
 
+// per-thread pool of timing events (cycle kernel / dense kernel brackets)
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t get(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+};
+static thread_local EventPool t_events;
+
 static int cfg_nblk(const DevInfo& d, int n) {
   int maxb = std::min(GRID_MAX, d.sms * std::max(1, d.cycle_blocks_per_sm));
   int want = (n + 255) / 256;  // at least 256 rows per CTA
@@ -1353,9 +1370,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   hflag[0] = -1;
   hflag[1] = 0;
 
-  cudaEvent_t ev0, ev1;
-  cudaEventCreate(&ev0);
-  cudaEventCreate(&ev1);
+  cudaEvent_t ev0 = t_events.get(0), ev1 = t_events.get(1);
+  int launches = 0;
   cudaEventRecord(ev0, s);
   k_setup<<<1, NT, 0, s>>>(p.st, n, L.ld, cfg->m, cfg->k, cfg->max_iter, cfg->tol,
                            A->diag ? 1 : 0, nblk, p.rpb, k_eff, x0 ? 1 : 0, dflag);
@@ -1366,6 +1382,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   k_init<<<nblk, NT, 0, s>>>(p, x0);
   const size_t dsm = dense_smem_bytes();
   k_dense<<<1, NT, dsm, s>>>(p, P_INIT, 0, -1);
+  launches += 3;
   if (k_eff > 0) {
     // orth(U_in): CholQR pass 1 + pass 2 with QRCP(R)
     k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
@@ -1391,6 +1408,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     k_reduce<<<8, NT, 0, s>>>(p, 2, 0);
     k_project<<<nblk, NT, 0, s>>>(p);
     k_dense<<<1, NT, dsm, s>>>(p, P_PROJ_FIN, 0, -1);
+    launches += 21;
   }
   if (cudaGetLastError() != cudaSuccess) {
     release_slot(slot);
@@ -1410,13 +1428,17 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     if (vf[1]) break;
     while (enq < seen + LOOK) {
       cyc = enq;
+      cudaEventRecord(t_events.get(2 + 3 * (size_t)enq), s);
       cudaError_t e = cudaLaunchCooperativeKernel((void*)k_cycle, dim3(nblk), dim3(NT), cargs, 0, s);
       if (e != cudaSuccess) {
         result = SKR_ERR_CUDA;
         break;
       }
+      cudaEventRecord(t_events.get(3 + 3 * (size_t)enq), s);
       k_dense<<<1, NT, dsm, s>>>(p, P_CYCLE, 0, enq);
+      cudaEventRecord(t_events.get(4 + 3 * (size_t)enq), s);
       launch_combine(kt, p, nblk, 1, s);
+      launches += 3;
       ++enq;
     }
     if (result) break;
@@ -1456,21 +1478,24 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   }
   k_final_resid<<<nblk, NT, 0, s>>>(p);
   k_dense<<<1, NT, dsm, s>>>(p, P_FINAL, 0, -1);
+  launches += 3;  // incl. k_setup
   cudaEventRecord(ev1, s);
   if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess)
     result = SKR_ERR_CUDA;
   release_slot(slot);
-  if (result) {
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    return result;
-  }
+  if (result) return result;
   State hs;
   cudaMemcpy(&hs, p.st, offsetof(State, kept), cudaMemcpyDeviceToHost);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
+  double cyc_ms = 0.0, den_ms = 0.0;
+  for (int c2 = 0; c2 < enq; ++c2) {
+    float a = 0.f, b2 = 0.f;
+    cudaEventElapsedTime(&a, t_events.get(2 + 3 * (size_t)c2), t_events.get(3 + 3 * (size_t)c2));
+    cudaEventElapsedTime(&b2, t_events.get(3 + 3 * (size_t)c2), t_events.get(4 + 3 * (size_t)c2));
+    cyc_ms += a;
+    den_ms += b2;
+  }
   if (hs.abort_flag) return SKR_ERR_TIMEOUT;
   memset(rep, 0, sizeof(*rep));
   rep->iterations = hs.iters;
@@ -1490,6 +1515,10 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   rep->bnorm = hs.bnorm;
   rep->device_ms = ms;
   rep->spmv_ortho_bytes = hs.step_bytes;
+  rep->cycle_kernel_ms = cyc_ms;
+  rep->dense_kernel_ms = den_ms;
+  rep->launches = launches;
+  rep->arnoldi_steps = hs.steps;
   if (hist && hist_cap > 0)
     cudaMemcpy(hist, p.hist, sizeof(double) * std::min(hist_cap, hs.hist_len),
                cudaMemcpyDeviceToHost);

@@ -27,7 +27,18 @@ from .gcrodr import engine_for
 from .gmres import SolverConfig
 from .sparse import DeviceCsr
 
-__all__ = ["SequenceResult", "solve_sequence", "chunk_positions"]
+__all__ = ["SequenceResult", "ChainState", "solve_sequence", "chunk_positions"]
+
+
+@dataclass
+class ChainState:
+    """Where a chain stands between calls: the engine whose workspace holds
+    the last recycle U (device pointer, leading dimension, columns)."""
+
+    engine: object = None
+    U_ptr: object = None
+    ld: int = 0
+    k: int = 0
 
 
 @dataclass
@@ -41,6 +52,11 @@ class SequenceResult:
     warn_bits: list = field(default_factory=list)
     spmv_ortho_bytes: float = 0.0
     x: list = field(default_factory=list)
+    launches: int = 0
+    cycle_kernel_ms: float = 0.0
+    dense_kernel_ms: float = 0.0
+    arnoldi_steps: int = 0
+    chain: ChainState = None
     wall_s: float = 0.0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
@@ -83,7 +99,7 @@ def _upload(sysobj, jacobi: bool, stream):
 def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[int],
                    cfg: SolverConfig, precond: str = "none", *, positions: Sequence[int] = None,
                    keep_x: str = "host", stream=None, recycle_first=None,
-                   want_history: bool = False) -> SequenceResult:
+                   want_history: bool = False, chain: ChainState = None) -> SequenceResult:
     """Solve ``systems[order[p]]`` for p in ``positions`` (default: all) as one
     recycling chain. ``systems`` is a sequence of (A, b) or a callable idx ->
     (A, b) (lazy generation for large configs). ``keep_x``: "host" (x copied
@@ -109,7 +125,9 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
     eng = None
     k_prev = 0
     U_prev_ptr, ld_prev = None, 0
-    if recycle_first is not None and recycle_first.k > 0:
+    if chain is not None and chain.engine is not None:
+        eng, U_prev_ptr, ld_prev, k_prev = chain.engine, chain.U_ptr, chain.ld, chain.k
+    elif recycle_first is not None and recycle_first.k > 0:
         from .gcrodr import _colmajor_device
 
         Ud, ld_prev = _colmajor_device(recycle_first.U, recycle_first.U.shape[0])
@@ -136,6 +154,10 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
         res.k_out.append(int(rep.k_out))
         res.warn_bits.append(int(rep.warn_bits))
         res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
+        res.launches += int(rep.launches)
+        res.cycle_kernel_ms += float(rep.cycle_kernel_ms)
+        res.dense_kernel_ms += float(rep.dense_kernel_ms)
+        res.arnoldi_steps += int(rep.arnoldi_steps)
         if keep_x == "host":
             res.x.append(x.cpu().numpy())
             res.d2h_bytes += _nbytes(x)
@@ -148,4 +170,5 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
             ld_prev, k_prev = ld, k
     torch.cuda.synchronize()
     res.wall_s = time.perf_counter() - t0
+    res.chain = ChainState(eng, U_prev_ptr, ld_prev, k_prev)
     return res

@@ -19,7 +19,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["ParameterMatrix", "frobenius_distance", "greedy_sort", "greedy_sort_device",
+__all__ = ["ParameterMatrix", "frobenius_distance", "gather_distance_rows", "greedy_sort",
+           "greedy_sort_device",
            "sharded_greedy_sort", "row_shard"]
 
 
@@ -108,6 +109,21 @@ def row_shard(n: int, world: int, rank: int) -> tuple[int, int]:
     return r0, min(n, r0 + per)
 
 
+def gather_distance_rows(local, n_sys: int, group=None):
+    """All-gather row blocks [row_shard(rank)] of the distance matrix into the
+    full (n_sys, n_sys) matrix on every rank (NCCL on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    per = -(-n_sys // world)
+    pad = torch.zeros((per, n_sys), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    chunks = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(chunks, pad, group=group)
+    return torch.cat(chunks)[:n_sys].contiguous()
+
+
 def sharded_greedy_sort(flat_dev, group=None, stream=None) -> list[int]:
     """Multi-GPU greedy sort: D2 rows sharded by rank, NCCL all_gather, then the
     (deterministic, replicated) chain on every rank. Every rank holds all params."""
@@ -125,17 +141,13 @@ def sharded_greedy_sort(flat_dev, group=None, stream=None) -> list[int]:
     isb = ctypes.c_int32()
     _lib.check(L.skr_sort_binary_check(flat_dev.data_ptr(), n_sys, P, v.ctypes.data,
                                        ctypes.byref(isb), ws.data_ptr(), need, sh), "binary_check")
-    per = -(-n_sys // world)
-    D2 = torch.zeros((per * world, n_sys), dtype=torch.float64, device="cuda")
     r0, r1 = row_shard(n_sys, world, rank)
-    local = D2[rank * per: rank * per + per]
+    local = torch.zeros((max(r1 - r0, 0), n_sys), dtype=torch.float64, device="cuda")
     if r1 > r0:
         _lib.check(L.skr_sort_dist2(flat_dev.data_ptr(), n_sys, P, r0, r1, isb.value,
                                     float(v[0]), float(v[1]), local.data_ptr(), ws.data_ptr(),
                                     need, sh), "dist2")
-    chunks = list(D2.split(per))
-    dist.all_gather(chunks, local.clone(), group=group)
-    D2 = torch.cat(chunks)[:n_sys].contiguous()
+    D2 = gather_distance_rows(local, n_sys, group)
     order = torch.zeros(n_sys, dtype=torch.int32, device="cuda")
     ncert = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.check(L.skr_sort_chain(D2.data_ptr(), flat_dev.data_ptr(), n_sys, P, isb.value,

@@ -1,0 +1,79 @@
+"""Multi-rank host logic under torch.distributed gloo on CPU (world_size 2):
+chunking of the sorted order across ranks and the sharded-distance gather
+that the NCCL path uses on the GPU box."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import skr_oracle as orc
+        from paper_2401_09516_b200.sequence import chunk_positions
+        from paper_2401_09516_b200.sorting import gather_distance_rows, row_shard
+
+        rng = np.random.default_rng(0)
+        flat = rng.standard_normal((37, 19))
+        n = flat.shape[0]
+        r0, r1 = row_shard(n, world, rank)
+        # local rows of the squared-distance matrix (what skr_sort_dist2 fills)
+        local = ((flat[r0:r1, None, :] - flat[None, :, :]) ** 2).sum(-1)
+        D2 = gather_distance_rows(torch.from_numpy(local), n, group=None)
+        full = ((flat[:, None, :] - flat[None, :, :]) ** 2).sum(-1)
+        ok_gather = bool(np.allclose(D2.numpy(), full))
+        # replicated greedy chain from the gathered matrix == oracle order
+        order = orc.greedy_order_from_d2(D2.numpy())
+        ok_order = order == orc.greedy_order(flat)
+        pos = list(chunk_positions(1024, world, rank))
+        q.put((rank, ok_gather, ok_order, pos[0], pos[-1], len(pos)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_sort_and_chunks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    out = sorted(q.get(timeout=10) for _ in range(world))
+    assert all(o[1] and o[2] for o in out)
+    # chunks are disjoint, contiguous and cover the batch
+    assert out[0][3] == 0 and out[0][4] + 1 == out[1][3] and out[1][4] == 1023
+    assert out[0][5] + out[1][5] == 1024
+
+
+def test_chunking_edge_cases():
+    from paper_2401_09516_b200.sequence import chunk_positions
+    from paper_2401_09516_b200.sorting import row_shard
+
+    for n, w in ((10, 3), (4096, 8), (5, 8), (1, 1)):
+        cov = []
+        for r in range(w):
+            cov += list(chunk_positions(n, w, r))
+            a, b = row_shard(n, w, r)
+            assert 0 <= a <= b <= n
+        assert cov == list(range(n))

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(PKG, "libskr.so")
 EXPORTS = (
     "skr_version", "skr_status_string", "skr_device_info", "skr_spmv", "skr_residual",
     "skr_gcrodr_workspace_bytes", "skr_gcrodr_solve", "skr_gcrodr_recycle_view",
+    "skr_gcrodr_profile",
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
     "skr_greedy_sort", "skr_dense_hr_first", "skr_dense_hr_next",
 )
@@ -74,6 +75,7 @@ def _declare(L):
         "skr_gcrodr_recycle_view": ([P, c_size_t, c_int32, c_int32, c_int32, POINTER(c_void_p),
                                      POINTER(c_void_p), POINTER(c_int32), POINTER(c_int32)],
                                     c_int32),
+        "skr_gcrodr_profile": ([P, c_size_t, c_int32, c_int32, c_int32, P], c_int32),
         "skr_sort_workspace_bytes": ([c_int32, c_int64], c_size_t),
         "skr_sort_binary_check": ([P, c_int32, c_int64, P, POINTER(c_int32), P, c_size_t, P],
                                   c_int32),

@@ -68,10 +68,14 @@ struct State {
   int iters, kc, kc_prev, k_new, converged, done, brk, ran, upd, j, cycles, defl_steps;
   int hist_len, nchecks, warn, status, abort_flag, zero_rhs, fallback, ncol_a, ncol_b, r_tmp,
       cm_mode, cm_nin_u, cm_nin_c, cm_nv, cm_nout_u, cm_nout_c, ncol_orig;
-  unsigned bar_count, bar_gen;
+  unsigned bar_count, bar_pad0[63];  // barrier words on separate 256-byte lines:
+  unsigned bar_gen, bar_pad1[63];    // pollers of bar_gen must not contend with arrivals
   int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
+  double acc[3 * PV_STEP];  // triple-buffered cross-CTA accumulators (k_cycle)
   int steps, pad2;    // Arnoldi steps executed
+  long long prof[32]; // [0,16) dense-kernel phase clocks (recycle.h SKR_PHASE),
+                      // [16,24) k_cycle phase clocks of CTA 0
   int kept[KMAX];
   // per-cycle small data
   double H[LDH * MMAX];
@@ -516,10 +520,20 @@ struct CycleSmem {
   double bp[KMAX];           // first-pass B column
   double dk[KMAX], cr[KMAX];
   double y[KMAX + MMAX];
+  double hcol[MMAX + 2];     // column being finalised (Givens in place)
   double sc[16];             // scalars
-  double bred[NW];
+  double bred[3 * NW];
   int flag;
 };
+
+#define CPROF(idx)                                                \
+  do {                                                            \
+    if (blk == 0 && tid == 0) {                                   \
+      long long _t = clock64();                                   \
+      st->prof[16 + (idx)] += _t - cprof_t;                       \
+      cprof_t = _t;                                               \
+    }                                                             \
+  } while (0)
 
 #define CYCLE_SYNC()                                              \
   do {                                                            \
@@ -532,10 +546,18 @@ struct CycleSmem {
     }                                                             \
   } while (0)
 
-__global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
+constexpr int GT_COLS = KMAX * 2 + MMAX + 1;
+constexpr size_t CYCLE_DSMEM_FIXED =
+    sizeof(double) * (16 * GT_COLS + MMAX * (MMAX + 1) / 2 + KMAX * MMAX);
+
+__global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
   State* st = p.st;
   __shared__ CycleSmem S;
-  __shared__ double gtile[16][KMAX * 2 + MMAX + 1];
+  extern __shared__ double cdyn[];
+  double(*gtile)[GT_COLS] = reinterpret_cast<double(*)[GT_COLS]>(cdyn);
+  double* Rsm = cdyn + 16 * GT_COLS;                // packed R (Givens-rotated H)
+  double* Bsm = Rsm + MMAX * (MMAX + 1) / 2;        // B, ld KMAX
+  int* csr_rp = reinterpret_cast<int*>(Bsm + KMAX * MMAX);  // cached CSR slice (optional)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int blk = blockIdx.x, nblk = p.nblk;
   if (st->done) {
@@ -554,6 +576,36 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
   const double beta = st->rnorm;
   const int r0 = blk * p.rpb, r1 = min(n, r0 + p.rpb);
   double* Qb = colC(p, kcap - kc);  // [C | V_0 ...] contiguous
+  // ---- cache this CTA's CSR slice in shared memory when it fits ---------------
+  bool csr_local = false;
+  int* lci = nullptr;
+  double* lav = nullptr;
+  if (csr_cap > 0 && r1 > r0) {
+    const int e0 = __ldg(p.rp + r0), e1 = __ldg(p.rp + r1);
+    const int rows = r1 - r0, nz = e1 - e0;
+    const size_t off_ci = (size_t)(rows + 1);
+    const size_t off_av = ((off_ci + nz) * sizeof(int) + 7) / 8;  // in doubles
+    if ((off_av + nz) * sizeof(double) <= (size_t)csr_cap) {
+      csr_local = true;
+      lci = csr_rp + off_ci;
+      lav = reinterpret_cast<double*>(csr_rp) + off_av;
+      for (int q = tid; q <= rows; q += NT) csr_rp[q] = __ldg(p.rp + r0 + q) - e0;
+      for (int q = tid; q < nz; q += NT) {
+        lci[q] = __ldg(p.ci + e0 + q);
+        lav[q] = __ldg(p.av + e0 + q);
+      }
+    }
+    __syncthreads();
+  }
+  auto row_dot = [&](const double* xv, int row) -> double {
+    if (csr_local) {
+      int a0 = csr_rp[row - r0], a1 = csr_rp[row - r0 + 1];
+      double acc = 0.0;
+      for (int q = a0; q < a1; ++q) acc = __dadd_rn(acc, __dmul_rn(lav[q], xv[lci[q]]));
+      return acc;
+    }
+    return csr_row(p.rp, p.ci, p.av, xv, row);
+  };
   const size_t ld = p.ld;
   unsigned* bc = &st->bar_count;
   unsigned* bg = &st->bar_gen;
@@ -578,12 +630,16 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
     st->dk[tid] = S.dk[tid];
     st->cr[tid] = S.cr[tid];
   }
+  if (blk == 0)
+    for (int v = tid; v < 3 * PV_STEP; v += NT) st->acc[v] = 0.0;
+  int red_idx = 0;
   CYCLE_SYNC();
 
   int j = 0;
   bool brk = false;
   double wn0_pending = 0.0;  // ||w - C C^T w|| / eta of the pending vector's step
   double hres = beta;
+  long long cprof_t = clock64();
   for (int t = 0; t <= s; ++t) {
     const bool do_spmv = (t < s);
     const int pb = kc + t;  // final basis columns [C | v_0..v_{t-1}]
@@ -602,7 +658,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
       if (row < r1) {
         wv = Vt[row];
         if (do_spmv) {
-          zv = csr_row(p.rp, p.ci, p.av, Vt, row);
+          zv = row_dot(Vt, row);
           if (p.dg) zv = __ddiv_rn(zv, __ldg(p.dg + row));
           p.z[row] = zv;
         }
@@ -632,54 +688,87 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
       }
       __syncthreads();
     }
-    // partial layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)
+    // cross-CTA sums by fp64 red.add into a triple-buffered accumulator
+    // (layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)); every CTA then
+    // reads the same totals. Buffer (r+2)%3 is zeroed after barrier r: its
+    // last readers finished before they arrived there.
+    double* accb = st->acc + (size_t)(red_idx % 3) * PV_STEP;
 #pragma unroll
     for (int q = 0; q < QMAX; ++q) {
       int col = warp + q * NW;
-      double sa = acc_a[q], sb = acc_b[q];
-      for (int o = 16; o > 0; o >>= 1) {
-        sa += __shfl_xor_sync(0xffffffffu, sa, o);
-        sb += __shfl_xor_sync(0xffffffffu, sb, o);
-      }
-      if (col < pb && lane == 0) {
-        p.part[(size_t)(3 + col) * GRID_MAX + blk] = sa;
-        p.part[(size_t)(3 + pb + col) * GRID_MAX + blk] = sb;
-      }
-    }
-    {
-      double t_nu = block_sum(nu, S.bred);
-      double t_mu = block_sum(mu, S.bred);
-      double t_ze = block_sum(ze, S.bred);
-      if (tid == 0) {
-        p.part[0 * GRID_MAX + blk] = t_nu;
-        p.part[1 * GRID_MAX + blk] = t_mu;
-        p.part[2 * GRID_MAX + blk] = t_ze;
-      }
-    }
-    CYCLE_SYNC();
-    reduce_partials(p.part, GRID_MAX, nblk, 0, 3 + 2 * pb, S.red);
-    // ---- LS / control (identical in every CTA) ------------------------------
-    if (tid == 0) {
-      double nu_ = S.red[0], mu_ = S.red[1], ze_ = S.red[2];
-      const double* A_ = S.red + 3;
-      const double* BB = S.red + 3 + pb;
-      bool stop = false;
-      double eta = 1.0;
-      if (t >= 1) {
-        double aa = 0.0;
-        for (int c = 0; c < pb; ++c) aa += A_[c] * A_[c];
-        eta = sqrt(fmax(nu_ - aa, 0.0));
-        int i = t - 1;  // finalize column i
-        double hcol[MMAX + 1];
-        for (int q = 0; q <= i; ++q) hcol[q] = S.hp[q] + A_[kc + q];
-        hcol[i + 1] = eta;
-        brk = eta < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308);
-        if (blk == 0) {
-          for (int c = 0; c < kc; ++c) st->B[c + i * LDB] = S.bp[c] + A_[c];
-          for (int q = 0; q <= i + 1; ++q) st->H[q + i * LDH] = hcol[q];
-          for (int q = i + 2; q < LDH; ++q) st->H[q + i * LDH] = 0.0;
+      if (col < pb) {  // warp-uniform
+        double sa = acc_a[q], sb = acc_b[q];
+        for (int o = 16; o > 0; o >>= 1) {
+          sa += __shfl_xor_sync(0xffffffffu, sa, o);
+          sb += __shfl_xor_sync(0xffffffffu, sb, o);
         }
-        // Givens
+        if (lane == 0) {
+          if (t >= 1) atomicAdd(accb + 3 + col, sa);
+          if (do_spmv) atomicAdd(accb + 3 + pb + col, sb);
+        }
+      }
+    }
+    block_sum3(nu, mu, ze, S.bred);
+    if (tid == 0) {
+      atomicAdd(accb + 0, nu);
+      if (do_spmv) {
+        atomicAdd(accb + 1, mu);
+        atomicAdd(accb + 2, ze);
+      }
+    }
+    CPROF(0);
+    CYCLE_SYNC();
+    CPROF(1);
+    for (int v = tid; v < 3 + 2 * pb; v += NT) S.red[v] = accb[v];
+    if (blk == 0) {
+      double* old = st->acc + (size_t)((red_idx + 2) % 3) * PV_STEP;
+      for (int v = tid; v < PV_STEP; v += NT) old[v] = 0.0;
+    }
+    ++red_idx;
+    __syncthreads();
+    // ---- LS / control (identical in every CTA) ------------------------------
+    const double* A_ = S.red + 3;
+    const double* BB = S.red + 3 + pb;
+    {
+      double aa = 0.0, ab = 0.0, cc = 0.0;
+      for (int c = tid; c < pb; c += NT) {
+        double av = (t >= 1) ? A_[c] : 0.0, bv = BB[c];
+        aa += av * av;
+        ab += av * bv;
+        if (c < kc) cc += bv * bv;
+      }
+      block_sum3(aa, ab, cc, S.bred);
+      if (tid == 0) {
+        double eta0 = (t >= 1) ? sqrt(fmax(S.red[0] - aa, 0.0)) : 1.0;
+        S.sc[0] = eta0;
+        S.sc[4] = ab;
+        S.sc[5] = cc;
+        S.sc[2] = (t >= 1 && eta0 < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308)) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+    }
+    const double eta = S.sc[0];
+    brk = S.sc[2] != 0.0;
+    if (t >= 1) {
+      // final column i = t-1: first pass + reorthogonalisation coefficients
+      const int i = t - 1;
+      for (int q = tid; q <= i + 1; q += NT) S.hcol[q] = (q <= i) ? S.hp[q] + A_[kc + q] : eta;
+      for (int c = tid; c < kc; c += NT) {
+        double v = S.bp[c] + A_[c];
+        Bsm[c + i * KMAX] = v;
+        if (blk == 0) st->B[c + i * LDB] = v;
+      }
+      if (blk == 0)
+        for (int q = tid; q < LDH; q += NT)
+          st->H[q + i * LDH] = (q <= i) ? S.hp[q] + A_[kc + q] : (q == i + 1 ? eta : 0.0);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // Givens update of column i (sequential); other threads scale in parallel
+      bool stop = false;
+      if (t >= 1) {
+        const int i = t - 1;
+        double* hcol = S.hcol;
         for (int q = 0; q < i; ++q) {
           double tt = S.cs[q] * hcol[q] + S.sn[q] * hcol[q + 1];
           hcol[q + 1] = -S.sn[q] * hcol[q] + S.cs[q] * hcol[q + 1];
@@ -700,39 +789,33 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
         S.gv[i + 1] = -sn_ * S.gv[i];
         S.gv[i] = cs_ * S.gv[i];
         hres = fabs(S.gv[i + 1]);
-        if (blk == 0) {
-          for (int q = 0; q <= i; ++q) st->R[q + i * LDR] = hcol[q];
-          p.hist[st->hist_len + i] = hres;
-        }
+        if (blk == 0) p.hist[st->hist_len + i] = hres;
         stop = brk || hres <= abs_tol || t == s;
       }
-      S.sc[0] = eta;
       S.sc[1] = stop ? 1.0 : 0.0;
-      S.sc[2] = brk ? 1.0 : 0.0;
       if (!stop) {
-        // first pass coefficients of column t (w = z / eta)
-        double ab = 0.0;
-        if (t >= 1)
-          for (int c = 0; c < pb; ++c) ab += A_[c] * BB[c];
-        for (int c = 0; c < kc; ++c) S.bp[c] = BB[c] / eta;
-        for (int q = 0; q < t; ++q) S.hp[q] = BB[kc + q] / eta;
-        S.hp[t] = (mu_ - ab) / (eta * eta);
-        double cc2 = 0.0;
-        for (int c = 0; c < kc; ++c) cc2 += BB[c] * BB[c];
-        wn0_pending = sqrt(fmax(ze_ - cc2, 0.0)) / eta;
-        S.sc[3] = S.hp[t];
+        S.sc[3] = (S.red[1] - S.sc[4]) / (eta * eta);  // h_tt = (mu - a.bb) / eta^2
+        wn0_pending = sqrt(fmax(S.red[2] - S.sc[5], 0.0)) / eta;
+      }
+    } else {
+      for (int c = tid - 1; c < pb; c += NT - 1) {
+        S.a[c] = (t >= 1) ? A_[c] : 0.0;
+        S.bb[c] = BB[c] / eta;  // first-pass coefficients of the new column
       }
     }
     __syncthreads();
-    const double eta = S.sc[0];
     const bool stop = S.sc[1] != 0.0;
-    brk = S.sc[2] != 0.0;
-    // coefficient vectors for sweep 2
-    for (int c = tid; c < pb; c += NT) {
-      S.a[c] = (t >= 1) ? S.red[3 + c] : 0.0;
-      S.bb[c] = stop ? 0.0 : S.red[3 + pb + c] / eta;
+    if (t >= 1) {
+      const int i = t - 1;
+      const int base = i * (i + 1) / 2;  // packed upper-triangular R
+      for (int q = tid; q <= i; q += NT) Rsm[base + q] = S.hcol[q];
     }
-    __syncthreads();
+    if (!stop) {
+      for (int c = tid; c < kc; c += NT) S.bp[c] = S.bb[c];
+      for (int q = tid; q < t; q += NT) S.hp[q] = S.bb[kc + q];
+      if (tid == 0) S.hp[t] = S.sc[3];
+    }
+    CPROF(2);
     // ---- sweep 2: finish V_t, project the new vector into V_{t+1} ----------
     {
       const double htt = S.sc[3];
@@ -758,41 +841,43 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
     }
     if (stop) {
       j = t;
-      // CTA 0: y = R^-1 g (warp 0), y1 = (cr - B y2) / dk
-      if (blk == 0 && warp == 0) {
+      // every CTA: y2 = R^-1 g (warp 0, packed R in smem), y1 = (cr - B y2) / dk
+      if (warp == 0) {
         for (int q = lane; q < j; q += 32) S.y[kc + q] = S.gv[q];
         __syncwarp();
         for (int kk = j - 1; kk >= 0; --kk) {
-          double yk = S.y[kc + kk] / st->R[kk + kk * LDR];
+          const int bk = kk * (kk + 1) / 2;
+          double yk = S.y[kc + kk] / Rsm[bk + kk];
           __syncwarp();
-          for (int q = lane; q < kk; q += 32) S.y[kc + q] -= st->R[q + kk * LDR] * yk;
+          for (int q = lane; q < kk; q += 32) S.y[kc + q] -= Rsm[bk + q] * yk;
           if (lane == 0) S.y[kc + kk] = yk;
           __syncwarp();
         }
         for (int c = lane; c < kc; c += 32) {
           double sacc = S.cr[c];
-          for (int q = 0; q < j; ++q) sacc -= st->B[c + q * LDB] * S.y[kc + q];
+          for (int q = 0; q < j; ++q) sacc -= Bsm[c + q * KMAX] * S.y[kc + q];
           S.y[c] = sacc / S.dk[c];
         }
         __syncwarp();
-        for (int q = lane; q < kc + j; q += 32) st->y[q] = S.y[q];
+        if (blk == 0)
+          for (int q = lane; q < kc + j; q += 32) st->y[q] = S.y[q];
       }
       if (blk == 0 && tid == 0) {
         st->j = j;
         st->brk = brk ? 1 : 0;
         st->g[0] = hres;
       }
-      CYCLE_SYNC();
+      __syncthreads();
+      CPROF(7);
       break;
     }
+    CPROF(3);
     CYCLE_SYNC();
+    CPROF(4);
   }
 
-  // ---- x update: x += U (dk y1) + V y2 ---------------------------------------
-  for (int q = tid; q < kc + j; q += NT) {
-    double yv = st->y[q];
-    S.y[q] = (q < kc) ? yv * S.dk[q] : yv;
-  }
+  // ---- x update: x += U (dk y1) + V y2 (own rows: no grid barrier needed) ----
+  for (int q = tid; q < kc; q += NT) S.y[q] *= S.dk[q];
   __syncthreads();
   for (int row = r0 + tid; row < r1; row += NT) {
     double su = 0.0, sv = 0.0;
@@ -800,24 +885,31 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
     for (int v = 0; v < j; ++v) sv += colV(p, v)[row] * S.y[kc + v];
     p.x[row] = p.x[row] + (su + sv);
   }
+  CPROF(8);
   CYCLE_SYNC();
+  CPROF(9);
 
   // ---- explicit residual + cross-Gram partials -------------------------------
   double rr = 0.0;
   for (int row = r0 + tid; row < r1; row += NT) {
-    double rv = __dsub_rn(__ldg(p.b + row), csr_row(p.rp, p.ci, p.av, p.x, row));
+    double rv = __dsub_rn(__ldg(p.b + row), row_dot(p.x, row));
     if (p.dg) rv = __ddiv_rn(rv, __ldg(p.dg + row));
     p.r[row] = rv;
     rr += rv * rv;
   }
   const int mm = kc + j;
   if (defl) {
+    // cross-Gram partials What[:, :mm]^T Vhat over this CTA's rows, register-tiled:
+    // thread -> 4 (What cols) x 2 (Vhat cols) entries; 16-row tiles staged in smem.
     // staged columns: [U (kc) | C (kc) | V_0..V_{j-1}]
     const int ncs = 2 * kc + j;
-    const int ne = mm * mm;
-    double gacc[(MMAX * MMAX + NT - 1) / NT];
+    const int na = (mm + 3) / 4, nbb = (mm + 1) / 2;
+    const int nblkt = na * nbb;  // thread blocks of entries
+    double gacc[2][8];
 #pragma unroll
-    for (int q = 0; q < (MMAX * MMAX + NT - 1) / NT; ++q) gacc[q] = 0.0;
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) gacc[u][q] = 0.0;
     for (int t0 = r0; t0 < r1; t0 += 16) {
       for (int e = tid; e < 16 * ncs; e += NT) {
         int rrw = e % 16, c = e / 16;
@@ -829,31 +921,59 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < (MMAX * MMAX + NT - 1) / NT; ++q) {
-        int e = tid + q * NT;
-        if (e < ne) {
-          int a = e % mm, b = e / mm;
-          int ca = (a < kc) ? kc + a : 2 * kc + (a - kc);  // What col: C or V
-          int cb = (b < kc) ? b : 2 * kc + (b - kc);       // Vhat col: U or V
-          double sacc = 0.0;
+      for (int u = 0; u < 2; ++u) {
+        int tb = tid + u * NT;
+        if (tb < nblkt) {
+          int a0 = (tb % na) * 4, b0 = (tb / na) * 2;
+          int ca[4], cb[2];
 #pragma unroll
-          for (int rrw = 0; rrw < 16; ++rrw) sacc += gtile[rrw][ca] * gtile[rrw][cb];
-          gacc[q] += sacc;
+          for (int x = 0; x < 4; ++x) {
+            int a = min(a0 + x, mm - 1);
+            ca[x] = (a < kc) ? kc + a : 2 * kc + (a - kc);  // What col: C or V
+          }
+#pragma unroll
+          for (int y = 0; y < 2; ++y) {
+            int b = min(b0 + y, mm - 1);
+            cb[y] = (b < kc) ? b : 2 * kc + (b - kc);  // Vhat col: U or V
+          }
+#pragma unroll 4
+          for (int rrw = 0; rrw < 16; ++rrw) {
+            double wa[4], vb[2];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) wa[x] = gtile[rrw][ca[x]];
+#pragma unroll
+            for (int y = 0; y < 2; ++y) vb[y] = gtile[rrw][cb[y]];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+              for (int y = 0; y < 2; ++y) gacc[u][x * 2 + y] = fma(wa[x], vb[y], gacc[u][x * 2 + y]);
+          }
         }
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < (MMAX * MMAX + NT - 1) / NT; ++q) {
-      int e = tid + q * NT;
-      if (e < ne) p.part[(size_t)(8 + e) * GRID_MAX + blk] = gacc[q];
+    for (int u = 0; u < 2; ++u) {
+      int tb = tid + u * NT;
+      if (tb < nblkt) {
+        int a0 = (tb % na) * 4, b0 = (tb / na) * 2;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y) {
+            int a = a0 + x, b = b0 + y;
+            if (a < mm && b < mm) p.part[(size_t)(8 + a + b * mm) * GRID_MAX + blk] = gacc[u][x * 2 + y];
+          }
+      }
     }
   }
   {
     double t_rr = block_sum(rr, S.bred);
     if (tid == 0) p.part[blk] = t_rr;
   }
+  CPROF(10);
   CYCLE_SYNC();
+  CPROF(11);
   if (defl) {
     // distributed reduction of the cross-Gram: entry e handled by warp (e % (nblk*NW))
     int gw = blk * NW + warp;
@@ -885,6 +1005,8 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id) {
       if (defl) st->defl_steps += j;
       st->cycles += 1;
       st->ran = 1;
+      st->prof[21] += clock64() - cprof_t;  // tail: distributed Gram reduce + r norm
+      st->prof[22] += j + 1;                // sweep iterations
       // SURVEY 8(d) algorithmic bytes: per step B_spmv + 8N(2p+6), p = basis width
       double N = (double)n;
       double nnz = (double)(__ldg(p.rp + n));
@@ -1049,6 +1171,7 @@ __global__ void __launch_bounds__(NT) k_dense(Ptrs p, int prog, int arg, int cyc
     }
     case P_CYCLE: {
       if (!st->ran) break;
+      ar.prof = st->prof;
       int kc = st->kc, j = st->j;
       int warn = 0;
       int r;
@@ -1145,6 +1268,8 @@ __global__ void __launch_bounds__(NT) k_resid(int n, const int32_t* rp, const in
 // ---------------------------------------------------------------------------
 static size_t dense_smem_bytes() { return skrd::arena_doubles(NW) * sizeof(double); }
 
+constexpr size_t CSR_CAP_MAX = 32 * 1024;  // bytes of CSR slice cached per CTA
+
 struct DevInfo {
   int sms = 0;
   int cycle_blocks_per_sm = 0;
@@ -1172,8 +1297,12 @@ static int ensure_dev(DevInfo** out) {
     if (cudaFuncSetAttribute(k_dense_hr, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dense_smem_bytes()) != cudaSuccess)
       return SKR_ERR_CUDA;
+    if (cudaFuncSetAttribute(k_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(CYCLE_DSMEM_FIXED + CSR_CAP_MAX)) != cudaSuccess)
+      return SKR_ERR_CUDA;
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle, NT, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle, NT,
+                                                      CYCLE_DSMEM_FIXED + CSR_CAP_MAX) != cudaSuccess)
       return SKR_ERR_CUDA;
     d.cycle_blocks_per_sm = nb;
     const int combine_smem = 2 * LDC * KMAX * (int)sizeof(double);
@@ -1234,7 +1363,10 @@ static thread_local EventPool t_events;
 
 static int cfg_nblk(const DevInfo& d, int n) {
   int maxb = std::min(GRID_MAX, d.sms * std::max(1, d.cycle_blocks_per_sm));
-  int want = (n + 255) / 256;  // at least 256 rows per CTA
+  int rows_min = 256;  // at least this many rows per CTA
+  if (const char* e = getenv("SKR_ROWS_MIN")) rows_min = std::max(32, atoi(e));
+  int want = (n + rows_min - 1) / rows_min;
+  if (const char* e = getenv("SKR_NBLK")) want = std::max(1, atoi(e));
   return std::max(1, std::min(maxb, want));
 }
 
@@ -1362,6 +1494,16 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.rpb = (int)align_up((size_t)((n + nblk - 1) / nblk), 32);
   const int kt = L.kcap;
   const int k_eff = cfg->k == 0 ? 0 : k_in;
+  // CSR slice cache: sized from the mean row length with headroom; CTAs whose
+  // slice does not fit read the matrix from global memory instead.
+  size_t csr_cap = 0;
+  {
+    double per_row = (double)A->nnz / std::max(1, n);
+    size_t want = (size_t)((p.rpb + 1) * 4 + (per_row * p.rpb * 1.25 + 64) * 12 + 64);
+    if (want <= CSR_CAP_MAX && !getenv("SKR_NO_CSR_CACHE")) csr_cap = (want + 255) / 256 * 256;
+  }
+  const size_t cycle_dsmem = CYCLE_DSMEM_FIXED + csr_cap;
+  int csr_cap_i = (int)csr_cap;
 
   int* hflag = nullptr;
   int* dflag = nullptr;
@@ -1418,10 +1560,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const int LOOK = 2;
   int enq = 0, seen = 0;
   int result = SKR_OK;
-  void* cargs[2];
+  void* cargs[3];
   int cyc = 0;
   cargs[0] = &p;
   cargs[1] = &cyc;
+  cargs[2] = &csr_cap_i;
   auto t_last = std::chrono::steady_clock::now();
   while (true) {
     volatile int* vf = hflag;
@@ -1429,7 +1572,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     while (enq < seen + LOOK) {
       cyc = enq;
       cudaEventRecord(t_events.get(2 + 3 * (size_t)enq), s);
-      cudaError_t e = cudaLaunchCooperativeKernel((void*)k_cycle, dim3(nblk), dim3(NT), cargs, 0, s);
+      cudaError_t e =
+          cudaLaunchCooperativeKernel((void*)k_cycle, dim3(nblk), dim3(NT), cargs, cycle_dsmem, s);
       if (e != cudaSuccess) {
         result = SKR_ERR_CUDA;
         break;
@@ -1525,6 +1669,17 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   if (checks && checks_cap > 0)
     cudaMemcpy(checks, p.checks, sizeof(double) * 2 * std::min(checks_cap, hs.nchecks),
                cudaMemcpyDeviceToHost);
+  return SKR_OK;
+}
+
+int skr_gcrodr_profile(void* ws, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
+                       long long* out16) {
+  if (!ws || !out16) return SKR_ERR_ARG;
+  (void)ws_bytes;
+  Layout L = make_layout(n, m, k, 1);
+  State* st = (State*)((char*)ws + L.state);
+  if (cudaMemcpy(out16, st->prof, 32 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return SKR_ERR_CUDA;
   return SKR_OK;
 }
 

@@ -26,7 +26,20 @@ struct Arena {
   double* xwork;  // nw * 3 * DMAX
   double* red;    // 64
   int* iw;        // 8 * LDD
+  long long* prof;  // optional phase clocks (device profiling), may be null
 };
+
+// phase clock accumulation (thread 0 only): [0] products [1] LU + kappa
+// [2] solve [3] eig (Hessenberg + QR) [4] select + eigenvectors [5] QRCP(P)
+// [6] GP tail [7] QR iterations [8] bulge steps [9] calls
+#define SKR_PHASE(ar, c, idx, t0)                                  \
+  do {                                                            \
+    if ((ar).prof && (c).tid == 0) {                              \
+      long long _t = SKR_CLK();                                   \
+      (ar).prof[idx] += _t - (t0);                                \
+      (t0) = _t;                                                  \
+    }                                                             \
+  } while (0)
 
 SKR_HD size_t arena_doubles(int nw) {
   return (size_t)5 * LDD * LDD + 12 * LDD + (size_t)nw * 3 * DMAX + 64;
@@ -45,6 +58,7 @@ SKR_HD Arena make_arena(double* d, int* iw, int nw) {
   a.xwork = a.vec + 12 * LDD;
   a.red = a.xwork + (size_t)nw * 3 * DMAX;
   a.iw = iw;
+  a.prof = 0;
   return a;
 }
 
@@ -106,7 +120,8 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
   bsync();
   double* wr = ar.vec;
   double* wi = ar.vec + LDD;
-  if (eig_schur(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD) != 0) return -D_QR_NOCONV;
+  if (eig_schur(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.xwork) != 0)
+    return -D_QR_NOCONV;
   int ncols = select_basis(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, kk, m, ar.M4, LDD, ar.iw + LDD,
                            ar.xwork, ar.red);
   if (ncols < 0) return -D_LINALG_ERROR;
@@ -122,61 +137,81 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
   if (mm <= 0 || mm > DMAX) return -D_LINALG_ERROR;
   int kk = k < mm ? k : mm;
   int* piv = ar.iw;
+  long long t0 = SKR_CLK();
   gemm(c, true, ar.G, LDD, ar.G, LDD, ar.M1, LDD, mm, mm, mm + 1);   // lhs = G^T G
   gemm(c, true, ar.G, LDD, cross, ldx, ar.M2, LDD, mm, mm, mm);      // rhs = G[:mm]^T cross
   bsync();
+  SKR_PHASE(ar, c, 0, t0);
   double fn = fro_norm(c, ar.M2, LDD, mm, mm, ar.red);
-  copy_mat(c, ar.M2, LDD, ar.M4, LDD, mm, mm);  // keep rhs
-  bsync();
   int info = 0;
   lu_factor(c, ar.M2, LDD, mm, piv, &info);
   bool singular = info != 0;
+  // one LU solve for [I | lhs]: I at M3 columns [LDD-mm, LDD), lhs at M4[:, 0:mm)
+  // (M3 and M4 are adjacent, so the 2 mm right-hand sides are contiguous)
+  double* X = ar.M3 + (size_t)(LDD - mm) * LDD;
   if (!singular) {
     for (int e = c.tid; e < mm * mm; e += c.nt) {
       int i = e % mm, j = e / mm;
-      DA(ar.M3, LDD, i, j) = (i == j) ? 1.0 : 0.0;
+      DA(X, LDD, i, j) = (i == j) ? 1.0 : 0.0;
+      DA(ar.M4, LDD, i, j) = DA(ar.M1, LDD, i, j);
     }
     bsync();
-    lu_solve(c, ar.M2, LDD, mm, piv, ar.M3, LDD, mm);
-    double gn = fro_norm(c, ar.M3, LDD, mm, mm, ar.red);
+    lu_solve(c, ar.M2, LDD, mm, piv, X, LDD, 2 * mm);
+    double gn = fro_norm(c, X, LDD, mm, mm, ar.red);
     if (!(fn * gn < KAPPA_CERT)) {
       *warn |= W_JACOBI_SVD;
-      singular = svd_singular(c, ar, ar.M4, LDD, mm, ar.M3);
+      gemm(c, true, ar.G, LDD, cross, ldx, ar.M3, LDD, mm, mm, mm);  // rhs again
+      bsync();
+      singular = svd_singular(c, ar, ar.M3, LDD, mm, ar.M2);
     }
   }
+  SKR_PHASE(ar, c, 1, t0);
   if (singular) {
     *warn |= W_SINGULAR_CROSS;
-    // pinv(rhs) via Jacobi SVD: M4 <- U S, M3 <- V
+    // pinv(rhs) via Jacobi SVD: M3 <- U S, M2 <- V, M4 <- pinv, A = pinv lhs -> M4
+    gemm(c, true, ar.G, LDD, cross, ldx, ar.M3, LDD, mm, mm, mm);
+    bsync();
     double* sv = ar.vec + 8 * LDD;
-    jacobi_svd(c, ar.M4, LDD, mm, mm, ar.M3, LDD, sv, ar.red);
+    jacobi_svd(c, ar.M3, LDD, mm, mm, ar.M2, LDD, sv, ar.red);
     double mx = 0.0;
     for (int i = 0; i < mm; ++i) mx = sv[i] > mx ? sv[i] : mx;
     double cut = 1e-15 * mx;  // numpy pinv default rcond
-    // pinv = sum_i V(:,i) (a_i / s_i^2)^T over s_i > cut  -> M2
     for (int e = c.tid; e < mm * mm; e += c.nt) {
       int i = e % mm, j = e / mm;
-      double s = 0.0;
+      double sacc = 0.0;
       for (int q = 0; q < mm; ++q)
-        if (sv[q] > cut) s += DA(ar.M3, LDD, i, q) * DA(ar.M4, LDD, j, q) / (sv[q] * sv[q]);
-      DA(ar.M2, LDD, i, j) = s;
+        if (sv[q] > cut) sacc += DA(ar.M2, LDD, i, q) * DA(ar.M3, LDD, j, q) / (sv[q] * sv[q]);
+      DA(ar.M4, LDD, i, j) = sacc;
     }
     bsync();
-    gemm(c, false, ar.M2, LDD, ar.M1, LDD, ar.M4, LDD, mm, mm, mm);  // pinv @ lhs
+    gemm(c, false, ar.M4, LDD, ar.M1, LDD, ar.M3, LDD, mm, mm, mm);  // pinv @ lhs
     bsync();
-    copy_mat(c, ar.M4, LDD, ar.M1, LDD, mm, mm);
+    copy_mat(c, ar.M3, LDD, ar.M4, LDD, mm, mm);
     bsync();
-  } else {
-    lu_solve(c, ar.M2, LDD, mm, piv, ar.M1, LDD, mm);  // rhs^-1 lhs
   }
+  SKR_PHASE(ar, c, 2, t0);
   double* wr = ar.vec;
   double* wi = ar.vec + LDD;
-  if (eig_schur(c, ar.M1, LDD, mm, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD) != 0) return -D_QR_NOCONV;
-  int ncols = select_basis(c, ar.M1, LDD, mm, ar.M3, LDD, wr, wi, kk, mm, ar.M4, LDD,
+  hessenberg(c, ar.M4, LDD, mm, ar.M3, LDD, ar.vec + 2 * LDD);
+  SKR_PHASE(ar, c, 10, t0);
+  int est = hqr(c, ar.M4, LDD, mm, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.xwork);
+  if (ar.prof && c.tid == 0) {
+    ar.prof[7] += (long long)ar.vec[2 * LDD + 1];
+    ar.prof[8] += (long long)ar.vec[2 * LDD + 2];
+    ar.prof[9] += 1;
+    for (int q = 0; q < 4; ++q) ar.prof[11 + q] += (long long)ar.vec[2 * LDD + 3 + q];
+  }
+  SKR_PHASE(ar, c, 3, t0);
+  if (est != 0) return -D_QR_NOCONV;
+  int ncols = select_basis(c, ar.M4, LDD, mm, ar.M3, LDD, wr, wi, kk, mm, ar.M1, LDD,
                            ar.iw + LDD, ar.xwork, ar.red);
+  SKR_PHASE(ar, c, 4, t0);
   if (ncols < 0) return -D_LINALG_ERROR;
   int* jp = ar.iw + 6 * LDD;
-  return qrcp(c, ar.M4, LDD, mm, ncols, jp, ar.M2, LDD, RANK_RTOL, ar.vec + 2 * LDD,
-              ar.vec + 5 * LDD);
+  int r1 = qrcp(c, ar.M1, LDD, mm, ncols, jp, ar.M2, LDD, RANK_RTOL, ar.vec + 2 * LDD,
+                ar.vec + 5 * LDD);
+  SKR_PHASE(ar, c, 5, t0);
+  return r1;
 }
 
 // Common tail: GP = G P_o ((rows) x r1) -> QRCP -> Q, R, kept; Z = P_o[:,kept] R^-1.
@@ -242,7 +277,9 @@ SKR_HD int recycle_next(const Ctx& c, Arena& ar, const double* H, int ldh, const
   bsync();
   int r1 = hr_next(c, ar, mm, cross, ldx, k, warn);
   if (r1 <= 0) return r1 < 0 ? r1 : 0;
+  long long t0 = SKR_CLK();
   int r2 = gp_tail(c, ar, mm + 1, mm, r1, coefU, ldu, coefC, ldcc);
+  SKR_PHASE(ar, c, 6, t0);
   if (r2 <= 0) return 0;
   for (int e = c.tid; e < kc * r2; e += c.nt) {
     int i = e % kc, q = e / kc;

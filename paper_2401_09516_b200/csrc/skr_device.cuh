@@ -56,10 +56,10 @@ __device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, int* a
       atomicAdd(gen, 1u);
     } else {
       unsigned long long t0 = gtimer();
-      unsigned ns = 8;
+      unsigned polls = 0;
       while (*vgen == g) {
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
+        __nanosleep(polls < 64 ? 20 : 100);
+        ++polls;
         if (gtimer() - t0 > BARRIER_TIMEOUT_NS) {
           atomicExch(abort_flag, 1);
           break;
@@ -89,6 +89,29 @@ __device__ __forceinline__ void reduce_partials(const double* part, int pstride,
     if (lane == 0) out[v - v0] = s;
   }
   __syncthreads();
+}
+
+// Block sums of three values per thread (results valid in every thread).
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* s_red) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    s_red[3 * warp] = a;
+    s_red[3 * warp + 1] = b;
+    s_red[3 * warp + 2] = c;
+  }
+  __syncthreads();
+  a = b = c = 0.0;
+  for (int w = 0; w < NW; ++w) {
+    a += s_red[3 * w];
+    b += s_red[3 * w + 1];
+    c += s_red[3 * w + 2];
+  }
 }
 
 // Block sum of one value per thread (result valid in every thread).

@@ -42,6 +42,7 @@ constexpr int LDB = KMAX;              // ld of B
 constexpr int LDX = MMAX;              // ld of cross
 constexpr int LDC = KMAX + MMAX + 1;   // ld of coefficient matrices
 constexpr int LDK = KMAX;              // ld of small k x k matrices
+constexpr int ACC_STRIDE = 32;         // doubles between accumulators (256 B)
 
 enum Prog {
   P_INIT = 0,
@@ -72,11 +73,14 @@ struct State {
   unsigned bar_gen, bar_pad1[63];    // pollers of bar_gen must not contend with arrivals
   int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
-  double acc[3 * PV_STEP];  // triple-buffered cross-CTA accumulators (k_cycle)
   int steps, pad2;    // Arnoldi steps executed
   long long prof[32]; // [0,16) dense-kernel phase clocks (recycle.h SKR_PHASE),
                       // [16,24) k_cycle phase clocks of CTA 0
   int kept[KMAX];
+  // triple-buffered cross-CTA accumulators of k_cycle; value v of buffer b at
+  // acc[(b * PV_STEP + v) * ACC_STRIDE]: one value per 256-byte line so the
+  // fp64 red.add traffic of all CTAs spreads over the L2 slices
+  double acc[3 * PV_STEP * ACC_STRIDE];
   // per-cycle small data
   double H[LDH * MMAX];
   double B[LDB * MMAX];
@@ -631,7 +635,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     st->cr[tid] = S.cr[tid];
   }
   if (blk == 0)
-    for (int v = tid; v < 3 * PV_STEP; v += NT) st->acc[v] = 0.0;
+    for (int v = tid; v < 3 * PV_STEP; v += NT) st->acc[(size_t)v * ACC_STRIDE] = 0.0;
   int red_idx = 0;
   CYCLE_SYNC();
 
@@ -692,7 +696,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     // (layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)); every CTA then
     // reads the same totals. Buffer (r+2)%3 is zeroed after barrier r: its
     // last readers finished before they arrived there.
-    double* accb = st->acc + (size_t)(red_idx % 3) * PV_STEP;
+    double* accb = st->acc + (size_t)(red_idx % 3) * PV_STEP * ACC_STRIDE;
 #pragma unroll
     for (int q = 0; q < QMAX; ++q) {
       int col = warp + q * NW;
@@ -703,26 +707,26 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
           sb += __shfl_xor_sync(0xffffffffu, sb, o);
         }
         if (lane == 0) {
-          if (t >= 1) atomicAdd(accb + 3 + col, sa);
-          if (do_spmv) atomicAdd(accb + 3 + pb + col, sb);
+          if (t >= 1) red_add_f64(accb + (3 + col) * ACC_STRIDE, sa);
+          if (do_spmv) red_add_f64(accb + (3 + pb + col) * ACC_STRIDE, sb);
         }
       }
     }
     block_sum3(nu, mu, ze, S.bred);
     if (tid == 0) {
-      atomicAdd(accb + 0, nu);
+      red_add_f64(accb, nu);
       if (do_spmv) {
-        atomicAdd(accb + 1, mu);
-        atomicAdd(accb + 2, ze);
+        red_add_f64(accb + ACC_STRIDE, mu);
+        red_add_f64(accb + 2 * ACC_STRIDE, ze);
       }
     }
     CPROF(0);
     CYCLE_SYNC();
     CPROF(1);
-    for (int v = tid; v < 3 + 2 * pb; v += NT) S.red[v] = accb[v];
+    for (int v = tid; v < 3 + 2 * pb; v += NT) S.red[v] = accb[(size_t)v * ACC_STRIDE];
     if (blk == 0) {
-      double* old = st->acc + (size_t)((red_idx + 2) % 3) * PV_STEP;
-      for (int v = tid; v < PV_STEP; v += NT) old[v] = 0.0;
+      double* old = st->acc + (size_t)((red_idx + 2) % 3) * PV_STEP * ACC_STRIDE;
+      for (int v = tid; v < PV_STEP; v += NT) old[(size_t)v * ACC_STRIDE] = 0.0;
     }
     ++red_idx;
     __syncthreads();

@@ -42,33 +42,50 @@ __device__ __forceinline__ double csr_row(const int32_t* __restrict__ rp,
 // arriver resets the counter and bumps the generation. A spin longer than
 // BARRIER_TIMEOUT_NS sets *abort instead of hanging the GPU. Returns false
 // when the solve was aborted (uniform across the CTA).
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 __device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, int* abort_flag,
                                           unsigned nblk, int* s_flag) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = gen;
-    unsigned g = *vgen;
-    __threadfence();
+    unsigned g = ld_relaxed_gpu(gen);
+    fence_acq_rel_gpu();  // release this CTA's writes (block-scope ordered by bar.sync)
     unsigned arrived = atomicAdd(count, 1u);
     if (arrived == nblk - 1) {
       atomicExch(count, 0u);
-      __threadfence();
+      fence_acq_rel_gpu();
       atomicAdd(gen, 1u);
     } else {
       unsigned long long t0 = gtimer();
       unsigned polls = 0;
-      while (*vgen == g) {
+      while (ld_relaxed_gpu(gen) == g) {
         __nanosleep(polls < 64 ? 20 : 100);
-        ++polls;
-        if (gtimer() - t0 > BARRIER_TIMEOUT_NS) {
-          atomicExch(abort_flag, 1);
-          break;
+        if ((++polls & 255) == 0) {
+          if (gtimer() - t0 > BARRIER_TIMEOUT_NS) {
+            atomicExch(abort_flag, 1);
+            break;
+          }
+          if (ld_relaxed_gpu(reinterpret_cast<unsigned*>(abort_flag))) break;
         }
-        if (*(volatile int*)abort_flag) break;
       }
     }
-    __threadfence();
-    *s_flag = *(volatile int*)abort_flag;
+    fence_acq_rel_gpu();  // acquire the other CTAs' writes
+    *s_flag = (int)ld_relaxed_gpu(reinterpret_cast<unsigned*>(abort_flag));
   }
   __syncthreads();
   return *s_flag == 0;

@@ -81,6 +81,8 @@ struct State {
   // acc[(b * PV_STEP + v) * ACC_STRIDE]: one value per 256-byte line so the
   // fp64 red.add traffic of all CTAs spreads over the L2 slices
   double acc[3 * PV_STEP * ACC_STRIDE];
+  // cross-Gram accumulators (entry e at gacc[e * ACC_STRIDE]); zero between uses
+  double gacc[MMAX * MMAX * ACC_STRIDE];
   // per-cycle small data
   double H[LDH * MMAX];
   double B[LDB * MMAX];
@@ -195,6 +197,8 @@ __global__ void k_setup(State* st, int n, int ld, int m, int k, int max_iter, do
       host_flag[1] = 0;
     }
   }
+  // cross-Gram accumulators must start at zero (k_cycle re-zeroes after use)
+  for (int e = threadIdx.x; e < MMAX * MMAX; e += blockDim.x) st->gacc[(size_t)e * ACC_STRIDE] = 0.0;
 }
 
 // x = x0 or 0; r = M^-1 (b - A x) or M^-1 b; partials: |b|^2, |M^-1 b|^2, |r|^2
@@ -514,8 +518,8 @@ __global__ void __launch_bounds__(NT) k_combine(Ptrs p, int cycle_mode) {
 // the persistent Arnoldi-cycle kernel
 // ---------------------------------------------------------------------------
 struct CycleSmem {
-  double w[NT];
-  double z[NT];
+  double w[2 * NT];
+  double z[2 * NT];
   double red[PV_STEP];
   double a[KMAX + MMAX];     // reorthogonalisation coefficients of the pending vector
   double bb[KMAX + MMAX];    // first-pass coefficients of the new vector (scaled)
@@ -551,15 +555,16 @@ struct CycleSmem {
   } while (0)
 
 constexpr int GT_COLS = KMAX * 2 + MMAX + 1;
+constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
 constexpr size_t CYCLE_DSMEM_FIXED =
-    sizeof(double) * (16 * GT_COLS + MMAX * (MMAX + 1) / 2 + KMAX * MMAX);
+    sizeof(double) * (GT_COLS * GT_LD + MMAX * (MMAX + 1) / 2 + KMAX * MMAX);
 
 __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
   State* st = p.st;
   __shared__ CycleSmem S;
   extern __shared__ double cdyn[];
-  double(*gtile)[GT_COLS] = reinterpret_cast<double(*)[GT_COLS]>(cdyn);
-  double* Rsm = cdyn + 16 * GT_COLS;                // packed R (Givens-rotated H)
+  double* gtile = cdyn;                             // Gram tile, column-major, ld GT_LD
+  double* Rsm = cdyn + GT_COLS * GT_LD;             // packed R (Givens-rotated H)
   double* Bsm = Rsm + MMAX * (MMAX + 1) / 2;        // B, ld KMAX
   int* csr_rp = reinterpret_cast<int*>(Bsm + KMAX * MMAX);  // cached CSR slice (optional)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -610,6 +615,46 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     }
     return csr_row(p.rp, p.ci, p.av, xv, row);
   };
+  // two rows (either may be >= r1): same per-row summation order as row_dot,
+  // with the two rows' loads interleaved
+  auto row_dot2 = [&](const double* xv, int ra, int rb, double& za, double& zb) {
+    const bool va = ra < r1, vb = rb < r1;
+    int a0, a1, b0, b1;
+    const int* ci_;
+    const double* av_;
+    if (csr_local) {
+      a0 = va ? csr_rp[ra - r0] : 0;
+      a1 = va ? csr_rp[ra - r0 + 1] : 0;
+      b0 = vb ? csr_rp[rb - r0] : 0;
+      b1 = vb ? csr_rp[rb - r0 + 1] : 0;
+      ci_ = lci;
+      av_ = lav;
+    } else {
+      a0 = va ? __ldg(p.rp + ra) : 0;
+      a1 = va ? __ldg(p.rp + ra + 1) : 0;
+      b0 = vb ? __ldg(p.rp + rb) : 0;
+      b1 = vb ? __ldg(p.rp + rb + 1) : 0;
+      ci_ = p.ci;
+      av_ = p.av;
+    }
+    double sa = 0.0, sb = 0.0;
+    const int la = a1 - a0, lb = b1 - b0, lm = la > lb ? la : lb;
+    for (int q = 0; q < lm; ++q) {
+      double xa = 0.0, xb = 0.0, va_ = 0.0, vb_ = 0.0;
+      if (q < la) {
+        va_ = csr_local ? av_[a0 + q] : __ldg(av_ + a0 + q);
+        xa = xv[csr_local ? ci_[a0 + q] : __ldg(ci_ + a0 + q)];
+      }
+      if (q < lb) {
+        vb_ = csr_local ? av_[b0 + q] : __ldg(av_ + b0 + q);
+        xb = xv[csr_local ? ci_[b0 + q] : __ldg(ci_ + b0 + q)];
+      }
+      if (q < la) sa = __dadd_rn(sa, __dmul_rn(va_, xa));
+      if (q < lb) sb = __dadd_rn(sb, __dmul_rn(vb_, xb));
+    }
+    za = sa;
+    zb = sb;
+  };
   const size_t ld = p.ld;
   unsigned* bc = &st->bar_count;
   unsigned* bg = &st->bar_gen;
@@ -656,24 +701,32 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       acc_b[q] = 0.0;
     }
     double nu = 0.0, mu = 0.0, ze = 0.0;
-    for (int t0 = r0; t0 < r1; t0 += NT) {
-      int row = t0 + tid;
-      double wv = 0.0, zv = 0.0;
-      if (row < r1) {
-        wv = Vt[row];
-        if (do_spmv) {
-          zv = row_dot(Vt, row);
-          if (p.dg) zv = __ddiv_rn(zv, __ldg(p.dg + row));
-          p.z[row] = zv;
+    for (int t0 = r0; t0 < r1; t0 += 2 * NT) {
+      // two rows per thread, their CSR loads interleaved (memory-level parallelism)
+      const int ra = t0 + tid, rb = t0 + NT + tid;
+      double wa = 0.0, za = 0.0, wb = 0.0, zb = 0.0;
+      if (ra < r1) wa = Vt[ra];
+      if (rb < r1) wb = Vt[rb];
+      if (do_spmv) {
+        row_dot2(Vt, ra, rb, za, zb);
+        if (ra < r1) {
+          if (p.dg) za = __ddiv_rn(za, __ldg(p.dg + ra));
+          p.z[ra] = za;
+        }
+        if (rb < r1) {
+          if (p.dg) zb = __ddiv_rn(zb, __ldg(p.dg + rb));
+          p.z[rb] = zb;
         }
       }
-      nu += wv * wv;
-      mu += wv * zv;
-      ze += zv * zv;
-      S.w[tid] = wv;
-      S.z[tid] = zv;
+      nu += wa * wa + wb * wb;
+      mu += wa * za + wb * zb;
+      ze += za * za + zb * zb;
+      S.w[tid] = wa;
+      S.z[tid] = za;
+      S.w[NT + tid] = wb;
+      S.z[NT + tid] = zb;
       __syncthreads();
-      int nrow = min(NT, r1 - t0);
+      int nrow = min(2 * NT, r1 - t0);
 #pragma unroll
       for (int q = 0; q < QMAX; ++q) {
         int col = warp + q * NW;
@@ -824,23 +877,37 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     {
       const double htt = S.sc[3];
       double* Vn = colV(p, t + 1);
-      for (int row = r0 + tid; row < r1; row += NT) {
-        double wv = Vt[row];
-        double ta = 0.0, tb = 0.0;
-        const double* q0 = Qb + row;
-        if (t >= 1 || !stop) {
+      const bool need = (t >= 1 || !stop);
+      for (int ra = r0 + tid; ra < r1; ra += 2 * NT) {
+        // two rows per thread: all loads before any store
+        const int rb = ra + NT;
+        const bool vb = rb < r1;
+        const double* qa = Qb + ra;
+        const double* qb = Qb + (vb ? rb : ra);
+        double ta = 0.0, tb = 0.0, ua = 0.0, ub = 0.0;
+        if (need) {
           for (int c = 0; c < pb; ++c) {
-            double qv = q0[(size_t)c * ld];
-            ta += qv * S.a[c];
-            tb += qv * S.bb[c];
+            double xa = qa[(size_t)c * ld], xb = qb[(size_t)c * ld];
+            double ca = S.a[c], cb = S.bb[c];
+            ta += xa * ca;
+            tb += xa * cb;
+            ua += xb * ca;
+            ub += xb * cb;
           }
         }
-        double vt = wv;
+        double wa = Vt[ra], wb = vb ? Vt[rb] : 0.0;
+        double za = p.z[ra], zb = vb ? p.z[rb] : 0.0;
+        double vta = wa, vtb = wb;
         if (t >= 1) {
-          vt = brk ? 0.0 : (wv - ta) / eta;
-          Vt[row] = vt;
+          vta = brk ? 0.0 : (wa - ta) / eta;
+          vtb = brk ? 0.0 : (wb - ua) / eta;
+          Vt[ra] = vta;
+          if (vb) Vt[rb] = vtb;
         }
-        if (!stop) Vn[row] = p.z[row] / eta - tb - vt * htt;
+        if (!stop) {
+          Vn[ra] = za / eta - tb - vta * htt;
+          if (vb) Vn[rb] = zb / eta - ub - vtb * htt;
+        }
       }
     }
     if (stop) {
@@ -903,50 +970,58 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   }
   const int mm = kc + j;
   if (defl) {
-    // cross-Gram partials What[:, :mm]^T Vhat over this CTA's rows, register-tiled:
-    // thread -> 4 (What cols) x 2 (Vhat cols) entries; 16-row tiles staged in smem.
+    // cross-Gram What[:, :mm]^T Vhat over this CTA's rows, register-tiled: a
+    // thread owns entries (ai + x*na4, bi + y*nb2), x < 4, y < 2, so
+    // consecutive lanes read consecutive columns of a 32-row tile staged
+    // column-major with an odd leading dimension (conflict-free). Per-CTA sums
+    // go straight to the cross accumulators with fp64 red.add (one 256-byte
+    // line per entry).
     // staged columns: [U (kc) | C (kc) | V_0..V_{j-1}]
     const int ncs = 2 * kc + j;
-    const int na = (mm + 3) / 4, nbb = (mm + 1) / 2;
-    const int nblkt = na * nbb;  // thread blocks of entries
+    const int na4 = (mm + 3) / 4, nb2 = (mm + 1) / 2;
+    const int nblkt = na4 * nb2;  // thread blocks of entries
     double gacc[2][8];
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int q = 0; q < 8; ++q) gacc[u][q] = 0.0;
-    for (int t0 = r0; t0 < r1; t0 += 16) {
-      for (int e = tid; e < 16 * ncs; e += NT) {
-        int rrw = e % 16, c = e / 16;
+    int ca[2][4], cb[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int tb = tid + u * NT;
+      int ai = tb % na4, bi = tb / na4;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        int a = min(ai + x * na4, mm - 1);
+        ca[u][x] = ((a < kc) ? kc + a : 2 * kc + (a - kc)) * GT_LD;  // What col: C or V
+      }
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        int b = min(bi + y * nb2, mm - 1);
+        cb[u][y] = ((b < kc) ? b : 2 * kc + (b - kc)) * GT_LD;  // Vhat col: U or V
+      }
+    }
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+      for (int e = tid; e < 32 * ncs; e += NT) {
+        int rrw = e % 32, c = e / 32;
         int row = t0 + rrw;
         const double* col = (c < kc) ? colU(p, c)
                             : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc))
                                            : colV(p, c - 2 * kc);
-        gtile[rrw][c] = row < r1 ? col[row] : 0.0;
+        gtile[c * GT_LD + rrw] = row < r1 ? col[row] : 0.0;
       }
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         int tb = tid + u * NT;
         if (tb < nblkt) {
-          int a0 = (tb % na) * 4, b0 = (tb / na) * 2;
-          int ca[4], cb[2];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            int a = min(a0 + x, mm - 1);
-            ca[x] = (a < kc) ? kc + a : 2 * kc + (a - kc);  // What col: C or V
-          }
-#pragma unroll
-          for (int y = 0; y < 2; ++y) {
-            int b = min(b0 + y, mm - 1);
-            cb[y] = (b < kc) ? b : 2 * kc + (b - kc);  // Vhat col: U or V
-          }
 #pragma unroll 4
-          for (int rrw = 0; rrw < 16; ++rrw) {
+          for (int rrw = 0; rrw < 32; ++rrw) {
             double wa[4], vb[2];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) wa[x] = gtile[rrw][ca[x]];
+            for (int x = 0; x < 4; ++x) wa[x] = gtile[ca[u][x] + rrw];
 #pragma unroll
-            for (int y = 0; y < 2; ++y) vb[y] = gtile[rrw][cb[y]];
+            for (int y = 0; y < 2; ++y) vb[y] = gtile[cb[u][y] + rrw];
 #pragma unroll
             for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -960,13 +1035,14 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     for (int u = 0; u < 2; ++u) {
       int tb = tid + u * NT;
       if (tb < nblkt) {
-        int a0 = (tb % na) * 4, b0 = (tb / na) * 2;
+        int ai = tb % na4, bi = tb / na4;
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 2; ++y) {
-            int a = a0 + x, b = b0 + y;
-            if (a < mm && b < mm) p.part[(size_t)(8 + a + b * mm) * GRID_MAX + blk] = gacc[u][x * 2 + y];
+            int a = ai + x * na4, b = bi + y * nb2;
+            if (a < mm && b < mm)
+              red_add_f64(st->gacc + (size_t)(a + b * mm) * ACC_STRIDE, gacc[u][x * 2 + y]);
           }
       }
     }
@@ -979,19 +1055,14 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   CYCLE_SYNC();
   CPROF(11);
   if (defl) {
-    // distributed reduction of the cross-Gram: entry e handled by warp (e % (nblk*NW))
-    int gw = blk * NW + warp;
-    int ngw = nblk * NW;
-    for (int e = gw; e < mm * mm; e += ngw) {
-      const double* q = p.part + (size_t)(8 + e) * GRID_MAX;
-      double sacc = 0.0;
-      for (int b = lane; b < nblk; b += 32) sacc += q[b];
-      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-      if (lane == 0) {
-        int a = e % mm, b = e / mm;
-        double v = (b < kc) ? sacc * st->dk[b] : sacc;  // Vhat = [U diag(dk), V]
-        st->cross[a + b * LDX] = v;
-      }
+    // the cross accumulators are complete after the barrier; scale Vhat's U
+    // columns by dk (Vhat = [U diag(dk), V]) into st->cross, re-zero for next use
+    for (int e = blk * NT + tid; e < mm * mm; e += nblk * NT) {
+      int a = e % mm, b = e / mm;
+      double* g = st->gacc + (size_t)e * ACC_STRIDE;
+      double v = *g;
+      *g = 0.0;
+      st->cross[a + b * LDX] = (b < kc) ? v * st->dk[b] : v;
     }
   }
   if (blk == 0) {
@@ -1599,9 +1670,9 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
         // stream drained: either done (flag) or stalled; re-check
         if (vf[1] || vf[0] >= seen) break;
         // nothing pending and no progress flag: the state says done
-        State hs;
-        cudaMemcpy(&hs.done, &p.st->done, sizeof(int), cudaMemcpyDeviceToHost);
-        if (hs.done) {
+        int hdone = 0;
+        cudaMemcpy(&hdone, &p.st->done, sizeof(int), cudaMemcpyDeviceToHost);
+        if (hdone) {
           vf[1] = 1;
           break;
         }
@@ -1632,8 +1703,9 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     result = SKR_ERR_CUDA;
   release_slot(slot);
   if (result) return result;
-  State hs;
-  cudaMemcpy(&hs, p.st, offsetof(State, kept), cudaMemcpyDeviceToHost);
+  std::vector<char> hbuf(offsetof(State, kept));
+  cudaMemcpy(hbuf.data(), p.st, offsetof(State, kept), cudaMemcpyDeviceToHost);
+  const State& hs = *reinterpret_cast<const State*>(hbuf.data());
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
   double cyc_ms = 0.0, den_ms = 0.0;

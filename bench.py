@@ -49,6 +49,10 @@ def _args():
     ap.add_argument("--impl", default="skr", choices=["skr", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--stripe", type=int, default=16, help="systems per step")
+    ap.add_argument("--chains", type=int, default=1,
+                    help="independent recycling chains per GPU (contiguous sub-chunks)")
+    ap.add_argument("--free-sms", type=int, default=2,
+                    help="SMs the cycle kernel leaves free for other chains (chains > 1)")
     ap.add_argument("--n-systems", type=int, default=None, help="override batch size")
     ap.add_argument("--grid", type=int, default=None, help="override grid side (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -260,6 +264,11 @@ def run_skr(args):
     dev = torch.device("cuda", local)
     spec = _spec(args)
     S, K, W = args.stripe, args.steps, args.warmup
+    NC = max(1, args.chains)
+    if S % NC:
+        raise SystemExit(f"--stripe {S} must be a multiple of --chains {NC}")
+    if NC > 1:
+        os.environ["SKR_FREE_SMS"] = str(args.free_sms)
     cfg = skr.SolverConfig(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
     # ---- sort (sharded rows + all_gather when world > 1) -------------------
     flat = _params(spec)
@@ -300,8 +309,11 @@ def run_skr(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    sub = S // NC          # systems per chain per step
+    span = (W + K) * sub   # positions per chain (contiguous sub-chunk of this rank's chunk)
+
     def run_pass(systems, keep_x):
-        chain = None
+        states = [None] * NC
         per_step, stats = [], []
         u_at_timed = None
         for st in range(W + K):
@@ -309,18 +321,23 @@ def run_skr(args):
             barrier()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
-            res = skr.solve_sequence(systems, ident, cfg, spec.precond,
-                                     positions=range(st * S, (st + 1) * S), keep_x=keep_x,
-                                     chain=chain)
+            chunks = [list(range(c * span + st * sub, c * span + (st + 1) * sub))
+                      for c in range(NC)]
+            if NC == 1:
+                rl = [skr.solve_sequence(systems, ident, cfg, spec.precond, positions=chunks[0],
+                                         keep_x=keep_x, chain=states[0])]
+            else:
+                rl = skr.solve_chains(systems, ident, cfg, spec.precond, chunks, keep_x=keep_x,
+                                      states=states)
             ev1.record()
             barrier()
-            chain = res.chain
-            if st == W - 1 and chain is not None and chain.k > 0:
-                U, C, k, ld = chain.engine.recycle_views()
+            states = [r.chain for r in rl]
+            if st == W - 1 and states[0] is not None and states[0].k > 0:
+                U, C, k, ld = states[0].engine.recycle_views()
                 u_at_timed = U.cpu().numpy()
             if st >= W:
                 per_step.append(ev0.elapsed_time(ev1))
-                stats.append(res)
+                stats.extend(rl)
         return per_step, stats, u_at_timed
 
     clocks = _Clocks()
@@ -352,13 +369,13 @@ def run_skr(args):
         if world > 1:
             dist.all_reduce(tot_e, op=dist.ReduceOp.MAX)
         e2e = {"value": n_sys_timed / (float(tot_e.item()) / 1000.0), "unit": "systems/s",
-               "h2d_bytes_per_step": int(np.mean([r.h2d_bytes for r in stats_e])),
-               "d2h_bytes_per_step": int(np.mean([r.d2h_bytes for r in stats_e])),
+               "h2d_bytes_per_step": int(sum(r.h2d_bytes for r in stats_e) / K),
+               "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in stats_e) / K),
                "path": "solve_sequence(pinned host CSR+b) -> x to host, per stripe"}
     # ---- CPU baseline: oracle port on this host (rank 0, N = 1) ------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = _cpu_baseline(spec, host, W * S, u_timed, args.cpu_budget_s)
+        cpu = _cpu_baseline(spec, host, W * sub, u_timed, args.cpu_budget_s)
     if rank != 0:
         return
     out = {
@@ -366,7 +383,8 @@ def run_skr(args):
         "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator; DCT-sampled GRF, see DESIGN.md)",
-        "config": _config_dict(spec, S, world),
+        "config": dict(_config_dict(spec, S, world), chains_per_gpu=NC,
+                       free_sms=(args.free_sms if NC > 1 else 0)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_cycle (persistent DCGS2 Arnoldi cycle: SpMV + ortho)",

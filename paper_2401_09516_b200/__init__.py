@@ -24,7 +24,14 @@ from .precond import (
     ZeroPivotError,
     build_preconditioner,
 )
-from .sequence import ChainState, SequenceResult, chunk_positions, solve_sequence
+from .sequence import (
+    ChainState,
+    SequenceResult,
+    chunk_positions,
+    solve_chains,
+    solve_sequence,
+    split_chunks,
+)
 from .sorting import (
     ParameterMatrix,
     frobenius_distance,
@@ -42,5 +49,5 @@ __all__ = [
     "SolverConfig", "ZeroPivotError", "axpy", "build_preconditioner", "chunk_positions", "dot",
     "eye", "frobenius_distance", "gcrodr_solve", "gmres_solve", "greedy_sort",
     "greedy_sort_device", "harmonic_ritz_first_cycle", "harmonic_ritz_subsequent", "norm2",
-    "sharded_greedy_sort", "solve_sequence", "spmv",
+    "sharded_greedy_sort", "solve_chains", "solve_sequence", "split_chunks", "spmv",
 ]

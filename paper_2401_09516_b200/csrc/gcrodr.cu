@@ -1373,7 +1373,8 @@ static int ensure_dev(DevInfo** out) {
                              (int)dense_smem_bytes()) != cudaSuccess)
       return SKR_ERR_CUDA;
     if (cudaFuncSetAttribute(k_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(CYCLE_DSMEM_FIXED + CSR_CAP_MAX)) != cudaSuccess)
+                             (int)std::max(CYCLE_DSMEM_FIXED + CSR_CAP_MAX,
+                                           (size_t)120 * 1024)) != cudaSuccess)
       return SKR_ERR_CUDA;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle, NT,
@@ -1436,8 +1437,17 @@ struct EventPool {
 };
 static thread_local EventPool t_events;
 
+// Multi-chain mode (SKR_FREE_SMS > 0): the cycle kernel runs one CTA per SM on
+// all but SKR_FREE_SMS SMs, so the single-CTA dense kernels of other chains
+// (other streams) find free SMs and overlap this chain's Arnoldi cycle.
+static int free_sms() {
+  const char* e = getenv("SKR_FREE_SMS");
+  return e ? std::max(0, atoi(e)) : 0;
+}
+
 static int cfg_nblk(const DevInfo& d, int n) {
   int maxb = std::min(GRID_MAX, d.sms * std::max(1, d.cycle_blocks_per_sm));
+  if (free_sms() > 0) maxb = std::max(1, d.sms - free_sms());
   int rows_min = 256;  // at least this many rows per CTA
   if (const char* e = getenv("SKR_ROWS_MIN")) rows_min = std::max(32, atoi(e));
   int want = (n + rows_min - 1) / rows_min;
@@ -1577,7 +1587,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     size_t want = (size_t)((p.rpb + 1) * 4 + (per_row * p.rpb * 1.25 + 64) * 12 + 64);
     if (want <= CSR_CAP_MAX && !getenv("SKR_NO_CSR_CACHE")) csr_cap = (want + 255) / 256 * 256;
   }
-  const size_t cycle_dsmem = CYCLE_DSMEM_FIXED + csr_cap;
+  size_t cycle_dsmem = CYCLE_DSMEM_FIXED + csr_cap;
+  if (free_sms() > 0) cycle_dsmem = std::max(cycle_dsmem, (size_t)120 * 1024);  // 1 CTA / SM
   int csr_cap_i = (int)csr_cap;
 
   int* hflag = nullptr;

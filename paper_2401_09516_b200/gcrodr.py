@@ -142,15 +142,17 @@ class GcroDrEngine:
 _ENGINES: dict = {}
 
 
-def engine_for(n: int, cfg: SolverConfig, device=None) -> GcroDrEngine:
+def engine_for(n: int, cfg: SolverConfig, device=None, slot: int = 0) -> GcroDrEngine:
+    """Cached engine (device workspace) per (device, n, m, k, max_iter, slot);
+    concurrent chains use distinct slots."""
     import torch
 
     dev = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
-    key = (str(dev), int(n), cfg.m, cfg.k, cfg.max_iter)
+    key = (str(dev), int(n), cfg.m, cfg.k, cfg.max_iter, int(slot))
     eng = _ENGINES.get(key)
     if eng is None:
-        if len(_ENGINES) > 4:
+        if len(_ENGINES) > 16:
             _ENGINES.clear()
         eng = GcroDrEngine(n, cfg, dev)
         _ENGINES[key] = eng

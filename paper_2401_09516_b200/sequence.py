@@ -27,7 +27,8 @@ from .gcrodr import engine_for
 from .gmres import SolverConfig
 from .sparse import DeviceCsr
 
-__all__ = ["SequenceResult", "ChainState", "solve_sequence", "chunk_positions"]
+__all__ = ["SequenceResult", "ChainState", "solve_sequence", "solve_chains", "chunk_positions",
+           "split_chunks"]
 
 
 @dataclass
@@ -99,7 +100,8 @@ def _upload(sysobj, jacobi: bool, stream):
 def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[int],
                    cfg: SolverConfig, precond: str = "none", *, positions: Sequence[int] = None,
                    keep_x: str = "host", stream=None, recycle_first=None,
-                   want_history: bool = False, chain: ChainState = None) -> SequenceResult:
+                   want_history: bool = False, chain: ChainState = None,
+                   engine_slot: int = 0) -> SequenceResult:
     """Solve ``systems[order[p]]`` for p in ``positions`` (default: all) as one
     recycling chain. ``systems`` is a sequence of (A, b) or a callable idx ->
     (A, b) (lazy generation for large configs). ``keep_x``: "host" (x copied
@@ -137,7 +139,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
         dA, bt, nb = nxt
         res.h2d_bytes += nb
         if eng is None:
-            eng = engine_for(dA.n, cfg)
+            eng = engine_for(dA.n, cfg, slot=engine_slot)
         # prefetch the next system while this one solves
         if i + 1 < len(res.order):
             nxt = _upload(get(res.order[i + 1]), jacobi, side)
@@ -172,3 +174,49 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
     res.wall_s = time.perf_counter() - t0
     res.chain = ChainState(eng, U_prev_ptr, ld_prev, k_prev)
     return res
+
+
+def split_chunks(positions: Sequence[int], parts: int) -> list:
+    """Split a run of sorted positions into ``parts`` contiguous sub-chains."""
+    positions = list(positions)
+    per = -(-len(positions) // max(1, parts))
+    return [positions[i: i + per] for i in range(0, len(positions), per)]
+
+
+def solve_chains(systems, order, cfg: SolverConfig, precond: str, chunks: Sequence,
+                 keep_x: str = "host", states: Sequence = None, want_history: bool = False):
+    """Run several independent recycling chains concurrently on one GPU, one
+    host thread + CUDA stream + workspace each (the paper's chunked SKR,
+    PAPER.md:2149-2184, applied inside a GPU). Each chunk is a contiguous run
+    of sorted positions; chain i continues from ``states[i]`` if given. With
+    SKR_FREE_SMS > 0 one chain's single-SM dense update overlaps the others'
+    Arnoldi cycles. Returns one SequenceResult per chunk."""
+    import threading
+
+    import torch
+
+    _lib.require_cuda()
+    dev = torch.cuda.current_device()
+    states = list(states) if states is not None else [None] * len(chunks)
+    out = [None] * len(chunks)
+    errs = []
+
+    def work(i):
+        try:
+            torch.cuda.set_device(dev)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                out[i] = solve_sequence(systems, order, cfg, precond, positions=chunks[i],
+                                        keep_x=keep_x, stream=st, chain=states[i],
+                                        engine_slot=i, want_history=want_history)
+        except BaseException as e:  # surfaced below
+            errs.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(chunks))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out

@@ -517,9 +517,9 @@ __global__ void __launch_bounds__(NT) k_combine(Ptrs p, int cycle_mode) {
 // ---------------------------------------------------------------------------
 // the persistent Arnoldi-cycle kernel
 // ---------------------------------------------------------------------------
+constexpr int PVC = KMAX + MMAX;  // basis columns, upper bound
+
 struct CycleSmem {
-  double w[2 * NT];
-  double z[2 * NT];
   double red[PV_STEP];
   double a[KMAX + MMAX];     // reorthogonalisation coefficients of the pending vector
   double bb[KMAX + MMAX];    // first-pass coefficients of the new vector (scaled)
@@ -533,6 +533,67 @@ struct CycleSmem {
   double bred[3 * NW];
   int flag;
 };
+
+
+// Warp reduce-scatter of NV values per lane (butterfly: NV - 1 + 5 - log2 NV
+// shuffles). Returns the warp sum of v[(lane >> (5 - log2 NV)) & (NV - 1)];
+// the 32 / NV lanes of a group hold the same value.
+template <int NV>
+__device__ __forceinline__ double bfly(double (&v)[NV], int lane) {
+  const unsigned F = 0xffffffffu;
+  int off = 16;
+#pragma unroll
+  for (int h = NV / 2; h >= 1; h /= 2, off /= 2) {
+    const bool hi = lane & off;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      double send = hi ? v[k] : v[k + h], keep = hi ? v[k + h] : v[k];
+      v[k] = keep + __shfl_xor_sync(F, send, off);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (; off >= 1; off /= 2) r += __shfl_xor_sync(F, r, off);
+  return r;
+}
+template <int NV>
+__host__ __device__ constexpr int log2c() { return NV <= 1 ? 0 : 1 + log2c<NV / 2>(); }
+
+// z_i = (A x)[row_i] for R rows per lane, every row summed sequentially in
+// CSR order with round-to-nearest mul/add (bit-exact with scipy csr_matvec);
+// the R rows' loads are interleaved for memory-level parallelism. LOCAL: the
+// CTA's CSR slice is in shared memory (rp rebased to r0).
+template <int R, bool LOCAL>
+__device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const double* av,
+                                          const double* xv, const int (&row)[R],
+                                          const bool (&ok)[R], int r0, double (&z)[R]) {
+  int a0[R], len[R];
+  int lm = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int rr = LOCAL ? row[i] - r0 : row[i];
+    const int b0 = LOCAL ? rp[rr] : __ldg(rp + rr);
+    const int b1 = LOCAL ? rp[rr + 1] : __ldg(rp + rr + 1);
+    a0[i] = b0;
+    len[i] = ok[i] ? b1 - b0 : 0;
+    lm = max(lm, len[i]);
+    z[i] = 0.0;
+  }
+  for (int q = 0; q < lm; ++q) {
+    double a[R], x[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (q < len[i]) {
+        const int e = a0[i] + q;
+        a[i] = LOCAL ? av[e] : __ldg(av + e);
+        x[i] = xv[LOCAL ? ci[e] : __ldg(ci + e)];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (q < len[i]) z[i] = __dadd_rn(z[i], __dmul_rn(a[i], x[i]));
+  }
+}
 
 #define CPROF(idx)                                                \
   do {                                                            \
@@ -556,14 +617,19 @@ struct CycleSmem {
 
 constexpr int GT_COLS = KMAX * 2 + MMAX + 1;
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
+static_assert(GT_COLS * GT_LD >= NW * 2 * PVC, "sweep-1 partials alias the Gram tile");
 constexpr size_t CYCLE_DSMEM_FIXED =
     sizeof(double) * (GT_COLS * GT_LD + MMAX * (MMAX + 1) / 2 + KMAX * MMAX);
 
+// R = rows per lane in the Arnoldi sweeps: warp-owned tiles of 32 R consecutive
+// rows; every lane keeps its rows' w = V_t and z = op(V_t) in registers.
+template <int R>
 __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
   State* st = p.st;
   __shared__ CycleSmem S;
   extern __shared__ double cdyn[];
   double* gtile = cdyn;                             // Gram tile, column-major, ld GT_LD
+  double* sacc = cdyn;  // aliases gtile (sweep 1 only): per-warp dot partials [a | bb], 2 PVC each
   double* Rsm = cdyn + GT_COLS * GT_LD;             // packed R (Givens-rotated H)
   double* Bsm = Rsm + MMAX * (MMAX + 1) / 2;        // B, ld KMAX
   int* csr_rp = reinterpret_cast<int*>(Bsm + KMAX * MMAX);  // cached CSR slice (optional)
@@ -585,6 +651,10 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   const double beta = st->rnorm;
   const int r0 = blk * p.rpb, r1 = min(n, r0 + p.rpb);
   double* Qb = colC(p, kcap - kc);  // [C | V_0 ...] contiguous
+  constexpr int TR = 32 * R;
+  constexpr int CB = R >= 4 ? 4 : 8;         // sweep-1 basis columns per butterfly batch
+  constexpr int SW2_COLS = R >= 4 ? 4 : 8;   // sweep-2 basis columns per load batch
+  const int ntile = r1 > r0 ? (r1 - r0 + TR - 1) / TR : 0;
   // ---- cache this CTA's CSR slice in shared memory when it fits ---------------
   bool csr_local = false;
   int* lci = nullptr;
@@ -614,46 +684,6 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       return acc;
     }
     return csr_row(p.rp, p.ci, p.av, xv, row);
-  };
-  // two rows (either may be >= r1): same per-row summation order as row_dot,
-  // with the two rows' loads interleaved
-  auto row_dot2 = [&](const double* xv, int ra, int rb, double& za, double& zb) {
-    const bool va = ra < r1, vb = rb < r1;
-    int a0, a1, b0, b1;
-    const int* ci_;
-    const double* av_;
-    if (csr_local) {
-      a0 = va ? csr_rp[ra - r0] : 0;
-      a1 = va ? csr_rp[ra - r0 + 1] : 0;
-      b0 = vb ? csr_rp[rb - r0] : 0;
-      b1 = vb ? csr_rp[rb - r0 + 1] : 0;
-      ci_ = lci;
-      av_ = lav;
-    } else {
-      a0 = va ? __ldg(p.rp + ra) : 0;
-      a1 = va ? __ldg(p.rp + ra + 1) : 0;
-      b0 = vb ? __ldg(p.rp + rb) : 0;
-      b1 = vb ? __ldg(p.rp + rb + 1) : 0;
-      ci_ = p.ci;
-      av_ = p.av;
-    }
-    double sa = 0.0, sb = 0.0;
-    const int la = a1 - a0, lb = b1 - b0, lm = la > lb ? la : lb;
-    for (int q = 0; q < lm; ++q) {
-      double xa = 0.0, xb = 0.0, va_ = 0.0, vb_ = 0.0;
-      if (q < la) {
-        va_ = csr_local ? av_[a0 + q] : __ldg(av_ + a0 + q);
-        xa = xv[csr_local ? ci_[a0 + q] : __ldg(ci_ + a0 + q)];
-      }
-      if (q < lb) {
-        vb_ = csr_local ? av_[b0 + q] : __ldg(av_ + b0 + q);
-        xb = xv[csr_local ? ci_[b0 + q] : __ldg(ci_ + b0 + q)];
-      }
-      if (q < la) sa = __dadd_rn(sa, __dmul_rn(va_, xa));
-      if (q < lb) sb = __dadd_rn(sb, __dmul_rn(vb_, xb));
-    }
-    za = sa;
-    zb = sb;
   };
   const size_t ld = p.ld;
   unsigned* bc = &st->bar_count;
@@ -694,76 +724,86 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     const int pb = kc + t;  // final basis columns [C | v_0..v_{t-1}]
     double* Vt = colV(p, t);
     // ---- sweep 1: z = op(V_t); dots of V_t and z against the final basis --
-    double acc_a[QMAX], acc_b[QMAX];
-#pragma unroll
-    for (int q = 0; q < QMAX; ++q) {
-      acc_a[q] = 0.0;
-      acc_b[q] = 0.0;
-    }
+    // no block barrier inside: each warp streams its own tiles, the basis
+    // columns in batches of CB (CB R independent loads per lane in flight), and
+    // reduce-scatters the 2 CB partial dots of a batch with one butterfly.
+    double* sw = sacc + warp * 2 * PVC;
+    for (int c = lane; c < 2 * PVC; c += 32) sw[c] = 0.0;
+    __syncwarp();
     double nu = 0.0, mu = 0.0, ze = 0.0;
-    for (int t0 = r0; t0 < r1; t0 += 2 * NT) {
-      // two rows per thread, their CSR loads interleaved (memory-level parallelism)
-      const int ra = t0 + tid, rb = t0 + NT + tid;
-      double wa = 0.0, za = 0.0, wb = 0.0, zb = 0.0;
-      if (ra < r1) wa = Vt[ra];
-      if (rb < r1) wb = Vt[rb];
-      if (do_spmv) {
-        row_dot2(Vt, ra, rb, za, zb);
-        if (ra < r1) {
-          if (p.dg) za = __ddiv_rn(za, __ldg(p.dg + ra));
-          p.z[ra] = za;
-        }
-        if (rb < r1) {
-          if (p.dg) zb = __ddiv_rn(zb, __ldg(p.dg + rb));
-          p.z[rb] = zb;
-        }
-      }
-      nu += wa * wa + wb * wb;
-      mu += wa * za + wb * zb;
-      ze += za * za + zb * zb;
-      S.w[tid] = wa;
-      S.z[tid] = za;
-      S.w[NT + tid] = wb;
-      S.z[NT + tid] = zb;
-      __syncthreads();
-      int nrow = min(2 * NT, r1 - t0);
+    for (int tile = warp; tile < ntile; tile += NW) {
+      const int base = r0 + tile * TR + lane;
+      int row[R];
+      bool ok[R];
+      double w[R], z[R];
 #pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        int col = warp + q * NW;
-        if (col < pb) {
-          const double* Qc = Qb + (size_t)col * ld + t0;
-          double sa = 0.0, sb = 0.0;
-#pragma unroll 4
-          for (int rr = lane; rr < nrow; rr += 32) {
-            double qv = Qc[rr];
-            sa += qv * S.w[rr];
-            sb += qv * S.z[rr];
-          }
-          acc_a[q] += sa;
-          acc_b[q] += sb;
-        }
+      for (int i = 0; i < R; ++i) {
+        const int rr = base + 32 * i;
+        ok[i] = rr < r1;
+        row[i] = ok[i] ? rr : r1 - 1;
+        w[i] = Vt[row[i]];
       }
-      __syncthreads();
+      if (do_spmv) {
+        if (csr_local)
+          spmv_rows<R, true>(csr_rp, lci, lav, Vt, row, ok, r0, z);
+        else
+          spmv_rows<R, false>(p.rp, p.ci, p.av, Vt, row, ok, r0, z);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          if (p.dg) z[i] = __ddiv_rn(z[i], __ldg(p.dg + row[i]));
+          if (ok[i]) p.z[row[i]] = z[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) z[i] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        if (!ok[i]) w[i] = z[i] = 0.0;
+        nu += w[i] * w[i];
+        mu += w[i] * z[i];
+        ze += z[i] * z[i];
+      }
+      for (int c0 = 0; c0 < pb; c0 += CB) {
+        // all CB x R loads first (no branch: columns past pb re-read column
+        // pb - 1 and their sums are dropped), then the FMAs
+        double qv[CB][R];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+          const double* Qc = Qb + (size_t)min(c0 + cc, pb - 1) * ld + base;
+#pragma unroll
+          for (int i = 0; i < R; ++i) qv[cc][i] = ok[i] ? Qc[32 * i] : 0.0;
+        }
+        double v[2 * CB];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+          double dw = 0.0, dz = 0.0;
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            dw = fma(qv[cc][i], w[i], dw);
+            dz = fma(qv[cc][i], z[i], dz);
+          }
+          v[cc] = dw;
+          v[CB + cc] = dz;
+        }
+        const double tot = bfly<2 * CB>(v, lane);
+        constexpr int SH = 5 - log2c<2 * CB>();
+        const int idx = (lane >> SH) & (2 * CB - 1), col = c0 + (idx % CB);
+        if (!(lane & ((1 << SH) - 1)) && col < pb) sw[(idx / CB) * PVC + col] += tot;
+      }
     }
+    __syncthreads();
     // cross-CTA sums by fp64 red.add into a triple-buffered accumulator
     // (layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)); every CTA then
     // reads the same totals. Buffer (r+2)%3 is zeroed after barrier r: its
     // last readers finished before they arrived there.
     double* accb = st->acc + (size_t)(red_idx % 3) * PV_STEP * ACC_STRIDE;
+    for (int e = tid; e < 2 * pb; e += NT) {
+      const int which = e >= pb, col = which ? e - pb : e;
+      double sum = 0.0;
 #pragma unroll
-    for (int q = 0; q < QMAX; ++q) {
-      int col = warp + q * NW;
-      if (col < pb) {  // warp-uniform
-        double sa = acc_a[q], sb = acc_b[q];
-        for (int o = 16; o > 0; o >>= 1) {
-          sa += __shfl_xor_sync(0xffffffffu, sa, o);
-          sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        }
-        if (lane == 0) {
-          if (t >= 1) red_add_f64(accb + (3 + col) * ACC_STRIDE, sa);
-          if (do_spmv) red_add_f64(accb + (3 + pb + col) * ACC_STRIDE, sb);
-        }
-      }
+      for (int q = 0; q < NW; ++q) sum += sacc[q * 2 * PVC + which * PVC + col];
+      if (which ? do_spmv : (t >= 1)) red_add_f64(accb + (size_t)(3 + e) * ACC_STRIDE, sum);
     }
     block_sum3(nu, mu, ze, S.bred);
     if (tid == 0) {
@@ -878,35 +918,52 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       const double htt = S.sc[3];
       double* Vn = colV(p, t + 1);
       const bool need = (t >= 1 || !stop);
-      for (int ra = r0 + tid; ra < r1; ra += 2 * NT) {
-        // two rows per thread: all loads before any store
-        const int rb = ra + NT;
-        const bool vb = rb < r1;
-        const double* qa = Qb + ra;
-        const double* qb = Qb + (vb ? rb : ra);
-        double ta = 0.0, tb = 0.0, ua = 0.0, ub = 0.0;
+      // tiles in the reverse order of sweep 1 (and of the next sweep 1): the
+      // rows streamed last are still in L2 when this sweep starts on them
+      for (int rt = warp; rt < ntile; rt += NW) {
+        const int tile = ntile - 1 - rt;
+        const int base = r0 + tile * TR + lane;
+        bool ok[R];
+        double ta[R], tb[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          ok[i] = base + 32 * i < r1;
+          ta[i] = 0.0;
+          tb[i] = 0.0;
+        }
         if (need) {
-          for (int c = 0; c < pb; ++c) {
-            double xa = qa[(size_t)c * ld], xb = qb[(size_t)c * ld];
-            double ca = S.a[c], cb = S.bb[c];
-            ta += xa * ca;
-            tb += xa * cb;
-            ua += xb * ca;
-            ub += xb * cb;
+          for (int c0 = 0; c0 < pb; c0 += SW2_COLS) {
+            // SW2_COLS x R loads first; columns past pb get zero coefficients
+            double qv[SW2_COLS][R];
+#pragma unroll
+            for (int cc = 0; cc < SW2_COLS; ++cc) {
+              const double* Qc = Qb + (size_t)min(c0 + cc, pb - 1) * ld + base;
+#pragma unroll
+              for (int i = 0; i < R; ++i) qv[cc][i] = ok[i] ? Qc[32 * i] : 0.0;
+            }
+#pragma unroll
+            for (int cc = 0; cc < SW2_COLS; ++cc) {
+              const bool in = c0 + cc < pb;
+              const double ca = in ? S.a[c0 + cc] : 0.0, cb = in ? S.bb[c0 + cc] : 0.0;
+#pragma unroll
+              for (int i = 0; i < R; ++i) {
+                ta[i] = fma(qv[cc][i], ca, ta[i]);
+                tb[i] = fma(qv[cc][i], cb, tb[i]);
+              }
+            }
           }
         }
-        double wa = Vt[ra], wb = vb ? Vt[rb] : 0.0;
-        double za = p.z[ra], zb = vb ? p.z[rb] : 0.0;
-        double vta = wa, vtb = wb;
-        if (t >= 1) {
-          vta = brk ? 0.0 : (wa - ta) / eta;
-          vtb = brk ? 0.0 : (wb - ua) / eta;
-          Vt[ra] = vta;
-          if (vb) Vt[rb] = vtb;
-        }
-        if (!stop) {
-          Vn[ra] = za / eta - tb - vta * htt;
-          if (vb) Vn[rb] = zb / eta - ub - vtb * htt;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          if (!ok[i]) continue;
+          const int rr = base + 32 * i;
+          const double wv = Vt[rr], zv = p.z[rr];
+          double vt = wv;
+          if (t >= 1) {
+            vt = brk ? 0.0 : (wv - ta[i]) / eta;
+            Vt[rr] = vt;
+          }
+          if (!stop) Vn[rr] = zv / eta - tb[i] - vt * htt;
         }
       }
     }
@@ -1354,6 +1411,23 @@ struct DevInfo {
 static DevInfo g_dev[16];
 static std::mutex g_mu;
 
+// k_cycle instantiation for R rows per lane (1, 2, 4 or 8)
+static const void* cycle_kernel(int R) {
+  switch (R) {
+    case 1: return (const void*)k_cycle<1>;
+    case 2: return (const void*)k_cycle<2>;
+    default: return (const void*)k_cycle<4>;
+  }
+}
+
+// rows per lane: 1 for slices of at most NT rows, else 2 (larger slices loop
+// over tiles; R = 4 measured slower at N = 1M)
+static int cycle_rows_per_lane(int rpb) {
+  int R = rpb <= NT ? 1 : 2;
+  if (const char* e = getenv("SKR_CYCLE_R")) R = std::max(1, std::min(4, atoi(e)));
+  return R == 3 ? 4 : R;
+}
+
 static int ensure_dev(DevInfo** out) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return SKR_ERR_CUDA;
@@ -1372,14 +1446,19 @@ static int ensure_dev(DevInfo** out) {
     if (cudaFuncSetAttribute(k_dense_hr, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dense_smem_bytes()) != cudaSuccess)
       return SKR_ERR_CUDA;
-    if (cudaFuncSetAttribute(k_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)std::max(CYCLE_DSMEM_FIXED + CSR_CAP_MAX,
-                                           (size_t)120 * 1024)) != cudaSuccess)
-      return SKR_ERR_CUDA;
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle, NT,
-                                                      CYCLE_DSMEM_FIXED + CSR_CAP_MAX) != cudaSuccess)
-      return SKR_ERR_CUDA;
+    int nb = 1 << 30;
+    for (int v = 0; v < 3; ++v) {
+      const void* f = cycle_kernel(1 << v);
+      if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max(CYCLE_DSMEM_FIXED + CSR_CAP_MAX,
+                                             (size_t)120 * 1024)) != cudaSuccess)
+        return SKR_ERR_CUDA;
+      int nbv = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbv, f, NT,
+                                                        CYCLE_DSMEM_FIXED + CSR_CAP_MAX) != cudaSuccess)
+        return SKR_ERR_CUDA;
+      nb = std::min(nb, nbv);
+    }
     d.cycle_blocks_per_sm = nb;
     const int combine_smem = 2 * LDC * KMAX * (int)sizeof(double);
     cudaFuncSetAttribute(k_combine<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
@@ -1590,6 +1669,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   size_t cycle_dsmem = CYCLE_DSMEM_FIXED + csr_cap;
   if (free_sms() > 0) cycle_dsmem = std::max(cycle_dsmem, (size_t)120 * 1024);  // 1 CTA / SM
   int csr_cap_i = (int)csr_cap;
+  const void* cycle_fn = cycle_kernel(cycle_rows_per_lane(p.rpb));
 
   int* hflag = nullptr;
   int* dflag = nullptr;
@@ -1659,7 +1739,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
       cyc = enq;
       cudaEventRecord(t_events.get(2 + 3 * (size_t)enq), s);
       cudaError_t e =
-          cudaLaunchCooperativeKernel((void*)k_cycle, dim3(nblk), dim3(NT), cargs, cycle_dsmem, s);
+          cudaLaunchCooperativeKernel(cycle_fn, dim3(nblk), dim3(NT), cargs, cycle_dsmem, s);
       if (e != cudaSuccess) {
         result = SKR_ERR_CUDA;
         break;

@@ -85,9 +85,8 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
   int kk = k < m ? k : m;
   int* piv = ar.iw;
   double hsub = DA(H, ldh, m, m - 1);
-  for (int j_ = c.warp; j_ < m; j_ += c.nw)
-    for (int i_ = c.lane; i_ < m; i_ += c.ws) {
-    int i = 0 + i_, j = 0 + j_;
+  for (Flat2 f_(c, m, m); f_.ok(); f_.next()) {
+    int i = f_.i, j = f_.j;
     DA(ar.M2, LDD, i, j) = DA(H, ldh, j, i);  // Hs^T
     DA(ar.M1, LDD, i, j) = DA(H, ldh, i, j);  // Hs
   }
@@ -98,9 +97,8 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
   bool singular = info != 0;
   if (!singular) {
     // [e_m | I]
-    for (int j_ = c.warp; j_ < (m + 1); j_ += c.nw)
-      for (int i_ = c.lane; i_ < m; i_ += c.ws) {
-      int i = 0 + i_, j = 0 + j_;
+    for (Flat2 f_(c, m, (m + 1)); f_.ok(); f_.next()) {
+      int i = f_.i, j = f_.j;
       DA(ar.M3, LDD, i, j) = (j == 0) ? (i == m - 1 ? 1.0 : 0.0) : (i == j - 1 ? 1.0 : 0.0);
     }
     bsync();
@@ -152,9 +150,8 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
   // (M3 and M4 are adjacent, so the 2 mm right-hand sides are contiguous)
   double* X = ar.M3 + (size_t)(LDD - mm) * LDD;
   if (!singular) {
-    for (int j_ = c.warp; j_ < mm; j_ += c.nw)
-      for (int i_ = c.lane; i_ < mm; i_ += c.ws) {
-      int i = 0 + i_, j = 0 + j_;
+    for (Flat2 f_(c, mm, mm); f_.ok(); f_.next()) {
+      int i = f_.i, j = f_.j;
       DA(X, LDD, i, j) = (i == j) ? 1.0 : 0.0;
       DA(ar.M4, LDD, i, j) = DA(ar.M1, LDD, i, j);
     }
@@ -179,9 +176,8 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
     double mx = 0.0;
     for (int i = 0; i < mm; ++i) mx = sv[i] > mx ? sv[i] : mx;
     double cut = 1e-15 * mx;  // numpy pinv default rcond
-    for (int j_ = c.warp; j_ < mm; j_ += c.nw)
-      for (int i_ = c.lane; i_ < mm; i_ += c.ws) {
-      int i = 0 + i_, j = 0 + j_;
+    for (Flat2 f_(c, mm, mm); f_.ok(); f_.next()) {
+      int i = f_.i, j = f_.j;
       double sacc = 0.0;
       for (int q = 0; q < mm; ++q)
         if (sv[q] > cut) sacc += DA(ar.M2, LDD, i, q) * DA(ar.M3, LDD, j, q) / (sv[q] * sv[q]);
@@ -229,16 +225,14 @@ SKR_HD int gp_tail(const Ctx& c, Arena& ar, int rows, int cols, int r1, double* 
                 ar.vec + 5 * LDD);
   if (r2 <= 0) return 0;
   inv_upper(c, ar.M1, LDD, r2, ar.M4, LDD);
-  for (int j_ = c.warp; j_ < r2; j_ += c.nw)
-    for (int i_ = c.lane; i_ < cols; i_ += c.ws) {
-    int i = 0 + i_, j = 0 + j_;
+  for (Flat2 f_(c, cols, r2); f_.ok(); f_.next()) {
+    int i = f_.i, j = f_.j;
     double s = 0.0;
     for (int q = 0; q <= j; ++q) s += DA(ar.M2, LDD, i, jp[q]) * DA(ar.M4, LDD, q, j);
     DA(Zc, ldz, i, j) = s;
   }
-  for (int j_ = c.warp; j_ < r2; j_ += c.nw)
-    for (int i_ = c.lane; i_ < rows; i_ += c.ws) {
-    int i = 0 + i_, j = 0 + j_;
+  for (Flat2 f_(c, rows, r2); f_.ok(); f_.next()) {
+    int i = f_.i, j = f_.j;
     DA(Qc, ldq, i, j) = DA(ar.M3, LDD, i, j);
   }
   bsync();
@@ -253,9 +247,8 @@ SKR_HD int recycle_first(const Ctx& c, Arena& ar, const double* H, int ldh, int 
   int kk = k < j ? k : j;
   int r1 = hr_first(c, ar, H, ldh, j, kk, warn);
   if (r1 <= 0) return r1 < 0 ? r1 : 0;
-  for (int q_ = c.warp; q_ < j; q_ += c.nw)
-    for (int i_ = c.lane; i_ < (j + 1); i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, j + 1, j); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     DA(ar.G, LDD, i, q) = DA(H, ldh, i, q);
   }
   bsync();
@@ -270,9 +263,8 @@ SKR_HD int recycle_next(const Ctx& c, Arena& ar, const double* H, int ldh, const
                         int k, double* coefU, int ldu, double* coefC, int ldcc, int* warn) {
   int mm = kc + j;
   if (mm + 1 > LDD) return -D_LINALG_ERROR;
-  for (int q_ = c.warp; q_ < mm; q_ += c.nw)
-    for (int i_ = c.lane; i_ < (mm + 1); i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, mm + 1, mm); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     double v = 0.0;
     if (i < kc && q < kc)
       v = (i == q) ? dk[i] : 0.0;
@@ -289,9 +281,8 @@ SKR_HD int recycle_next(const Ctx& c, Arena& ar, const double* H, int ldh, const
   int r2 = gp_tail(c, ar, mm + 1, mm, r1, coefU, ldu, coefC, ldcc);
   SKR_PHASE(ar, c, 6, t0);
   if (r2 <= 0) return 0;
-  for (int q_ = c.warp; q_ < r2; q_ += c.nw)
-    for (int i_ = c.lane; i_ < kc; i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, kc, r2); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     DA(coefU, ldu, i, q) *= dk[i];
   }
   bsync();
@@ -320,9 +311,8 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
     perm[i] = i;
   }
   bsync();
-  for (int j_ = c.warp; j_ < k; j_ += c.nw)
-    for (int i_ = c.lane; i_ < k; i_ += c.ws) {
-    int i = 0 + i_, j = 0 + j_;
+  for (Flat2 f_(c, k, k); f_.ok(); f_.next()) {
+    int i = f_.i, j = f_.j;
     double den = dsq[i] * dsq[j];
     DA(S, LDD, i, j) = den > 0.0 ? DA(Gm, ldg, i, j) / den : 0.0;
     DA(R, LDD, i, j) = 0.0;
@@ -377,35 +367,30 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
       DA(R, LDD, i, q) = (q == i) ? rii : DA(S, LDD, i, q) / rii;
     bsync();
     int rem = k - i - 1;
-    for (int b_ = c.warp; b_ < rem; b_ += c.nw)
-      for (int a_ = c.lane; a_ < rem; a_ += c.ws) {
-      int a = i + 1 + a_, b = i + 1 + b_;
+    for (Flat2 f_(c, rem, rem); f_.ok(); f_.next()) {
+      int a = i + 1 + f_.i, b = i + 1 + f_.j;
       DA(S, LDD, a, b) -= DA(R, LDD, i, a) * DA(R, LDD, i, b);
     }
     bsync();
   }
   // unscale: R_true(:, q) = R(:, q) * dsq[perm[q]]
-  for (int q_ = c.warp; q_ < k; q_ += c.nw)
-    for (int i_ = c.lane; i_ < rank; i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, rank, k); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     DA(R, LDD, i, q) *= dsq[perm[q]];
   }
   bsync();
   if (rank > 0) inv_upper(c, R, LDD, rank, ar.M3, LDD);
-  for (int q_ = c.warp; q_ < rank; q_ += c.nw)
-    for (int i_ = c.lane; i_ < k; i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, k, rank); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     DA(T1, ldt, i, q) = 0.0;
   }
   bsync();
-  for (int q_ = c.warp; q_ < rank; q_ += c.nw)
-    for (int i_ = c.lane; i_ < rank; i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, rank, rank); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     DA(T1, ldt, perm[i], q) = DA(ar.M3, LDD, i, q);
   }
-  for (int q_ = c.warp; q_ < k; q_ += c.nw)
-    for (int i_ = c.lane; i_ < rank; i_ += c.ws) {
-    int i = 0 + i_, q = 0 + q_;
+  for (Flat2 f_(c, rank, k); f_.ok(); f_.next()) {
+    int i = f_.i, q = f_.j;
     DA(R1, ldr, i, perm[q]) = DA(R, LDD, i, q);
   }
   bsync();

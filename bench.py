@@ -49,10 +49,10 @@ def _args():
     ap.add_argument("--impl", default="skr", choices=["skr", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--stripe", type=int, default=16, help="systems per step")
-    ap.add_argument("--chains", type=int, default=1,
+    ap.add_argument("--chains", type=int, default=8,
                     help="independent recycling chains per GPU (contiguous sub-chunks)")
-    ap.add_argument("--free-sms", type=int, default=2,
-                    help="SMs the cycle kernel leaves free for other chains (chains > 1)")
+    ap.add_argument("--ctas-per-chain", type=int, default=None,
+                    help="CTAs of each chain's Arnoldi kernel (default: chain_grid_ctas)")
     ap.add_argument("--n-systems", type=int, default=None, help="override batch size")
     ap.add_argument("--grid", type=int, default=None, help="override grid side (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -267,8 +267,7 @@ def run_skr(args):
     NC = max(1, args.chains)
     if S % NC:
         raise SystemExit(f"--stripe {S} must be a multiple of --chains {NC}")
-    if NC > 1:
-        os.environ["SKR_FREE_SMS"] = str(args.free_sms)
+    gctas = skr.chain_grid_ctas(NC) if args.ctas_per_chain is None else args.ctas_per_chain
     cfg = skr.SolverConfig(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
     # ---- sort (sharded rows + all_gather when world > 1) -------------------
     flat = _params(spec)
@@ -328,7 +327,7 @@ def run_skr(args):
                                          keep_x=keep_x, chain=states[0])]
             else:
                 rl = skr.solve_chains(systems, ident, cfg, spec.precond, chunks, keep_x=keep_x,
-                                      states=states)
+                                      states=states, grid_ctas=gctas)
             ev1.record()
             barrier()
             states = [r.chain for r in rl]
@@ -384,7 +383,7 @@ def run_skr(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator; DCT-sampled GRF, see DESIGN.md)",
         "config": dict(_config_dict(spec, S, world), chains_per_gpu=NC,
-                       free_sms=(args.free_sms if NC > 1 else 0)),
+                       ctas_per_chain=gctas),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_cycle (persistent DCGS2 Arnoldi cycle: SpMV + ortho)",

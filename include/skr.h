@@ -50,12 +50,14 @@ typedef struct skr_csr {
   const double* diag;
 } skr_csr;
 
-/* SolverConfig (gmres.py:26-43). */
+/* SolverConfig (gmres.py:26-43) + one launch knob. */
 typedef struct skr_config {
   int32_t m;
   int32_t k;
   int32_t max_iter;
-  int32_t reserved;
+  int32_t grid_ctas; /* CTAs of the persistent Arnoldi kernel; 0 = fill the GPU.
+                        Callers running several chains concurrently on one GPU
+                        give each chain a share (e.g. 2 * SMs / chains * 2). */
   double tol;
 } skr_config;
 

@@ -28,6 +28,7 @@ from .sequence import (
     ChainState,
     SequenceResult,
     chunk_positions,
+    chain_grid_ctas,
     solve_chains,
     solve_sequence,
     split_chunks,
@@ -49,5 +50,5 @@ __all__ = [
     "SolverConfig", "ZeroPivotError", "axpy", "build_preconditioner", "chunk_positions", "dot",
     "eye", "frobenius_distance", "gcrodr_solve", "gmres_solve", "greedy_sort",
     "greedy_sort_device", "harmonic_ritz_first_cycle", "harmonic_ritz_subsequent", "norm2",
-    "sharded_greedy_sort", "solve_chains", "solve_sequence", "split_chunks", "spmv",
+    "sharded_greedy_sort", "chain_grid_ctas", "solve_chains", "solve_sequence", "split_chunks", "spmv",
 ]

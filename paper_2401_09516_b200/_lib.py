@@ -35,7 +35,7 @@ class SkrCsr(ctypes.Structure):
 
 class SkrConfig(ctypes.Structure):
     _fields_ = [("m", c_int32), ("k", c_int32), ("max_iter", c_int32),
-                ("reserved", c_int32), ("tol", c_double)]
+                ("grid_ctas", c_int32), ("tol", c_double)]
 
 
 class SkrReport(ctypes.Structure):

@@ -1450,8 +1450,7 @@ static int ensure_dev(DevInfo** out) {
     for (int v = 0; v < 3; ++v) {
       const void* f = cycle_kernel(1 << v);
       if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)std::max(CYCLE_DSMEM_FIXED + CSR_CAP_MAX,
-                                             (size_t)120 * 1024)) != cudaSuccess)
+                               (int)(CYCLE_DSMEM_FIXED + CSR_CAP_MAX)) != cudaSuccess)
         return SKR_ERR_CUDA;
       int nbv = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbv, f, NT,
@@ -1516,21 +1515,15 @@ struct EventPool {
 };
 static thread_local EventPool t_events;
 
-// Multi-chain mode (SKR_FREE_SMS > 0): the cycle kernel runs one CTA per SM on
-// all but SKR_FREE_SMS SMs, so the single-CTA dense kernels of other chains
-// (other streams) find free SMs and overlap this chain's Arnoldi cycle.
-static int free_sms() {
-  const char* e = getenv("SKR_FREE_SMS");
-  return e ? std::max(0, atoi(e)) : 0;
-}
-
-static int cfg_nblk(const DevInfo& d, int n) {
-  int maxb = std::min(GRID_MAX, d.sms * std::max(1, d.cycle_blocks_per_sm));
-  if (free_sms() > 0) maxb = std::max(1, d.sms - free_sms());
-  int rows_min = 256;  // at least this many rows per CTA
+// CTAs of the row-partitioned kernels: enough for >= SKR_ROWS_MIN (256) rows
+// each, at most what is co-resident on the GPU; `grid_ctas` > 0 (skr_config)
+// caps it so several concurrent chains share the SMs.
+static int cfg_nblk(const DevInfo& d, int n, int grid_ctas) {
+  const int maxb = std::min(GRID_MAX, d.sms * std::max(1, d.cycle_blocks_per_sm));
+  int rows_min = 256;
   if (const char* e = getenv("SKR_ROWS_MIN")) rows_min = std::max(32, atoi(e));
   int want = (n + rows_min - 1) / rows_min;
-  if (const char* e = getenv("SKR_NBLK")) want = std::max(1, atoi(e));
+  if (grid_ctas > 0) want = std::min(want, grid_ctas);
   return std::max(1, std::min(maxb, want));
 }
 
@@ -1625,7 +1618,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   if (!A || !b || !x || !cfg || !ws || !rep) return SKR_ERR_ARG;
   const int n = A->n;
   if (n <= 0 || cfg->m < 2 || cfg->k < 0 || cfg->k >= cfg->m || !(cfg->tol > 0) ||
-      cfg->max_iter < 1)
+      cfg->max_iter < 1 || cfg->grid_ctas < 0)
     return SKR_ERR_ARG;
   if (cfg->m + 1 > MMAX || cfg->k + 1 > KMAX) return SKR_ERR_UNSUPPORTED;
   if (k_in < 0 || k_in > cfg->k + 1 || (k_in > 0 && (!U_in || ldu < n))) return SKR_ERR_ARG;
@@ -1653,7 +1646,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.n = n;
   p.ld = L.ld;
   p.kcap = L.kcap;
-  const int nblk = cfg_nblk(*d, n);
+  const int nblk = cfg_nblk(*d, n, cfg->grid_ctas);
   p.nblk = nblk;
   p.rpb = (int)align_up((size_t)((n + nblk - 1) / nblk), 32);
   const int kt = L.kcap;
@@ -1667,7 +1660,6 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     if (want <= CSR_CAP_MAX && !getenv("SKR_NO_CSR_CACHE")) csr_cap = (want + 255) / 256 * 256;
   }
   size_t cycle_dsmem = CYCLE_DSMEM_FIXED + csr_cap;
-  if (free_sms() > 0) cycle_dsmem = std::max(cycle_dsmem, (size_t)120 * 1024);  // 1 CTA / SM
   int csr_cap_i = (int)csr_cap;
   const void* cycle_fn = cycle_kernel(cycle_rows_per_lane(p.rpb));
 

@@ -142,9 +142,11 @@ class GcroDrEngine:
 _ENGINES: dict = {}
 
 
-def engine_for(n: int, cfg: SolverConfig, device=None, slot: int = 0) -> GcroDrEngine:
+def engine_for(n: int, cfg: SolverConfig, device=None, slot: int = 0,
+               grid_ctas: int = 0) -> GcroDrEngine:
     """Cached engine (device workspace) per (device, n, m, k, max_iter, slot);
-    concurrent chains use distinct slots."""
+    concurrent chains use distinct slots and a ``grid_ctas`` share of the GPU
+    (0 = the whole GPU; skr_config.grid_ctas)."""
     import torch
 
     dev = torch.device(device) if device is not None else torch.device(
@@ -156,7 +158,7 @@ def engine_for(n: int, cfg: SolverConfig, device=None, slot: int = 0) -> GcroDrE
             _ENGINES.clear()
         eng = GcroDrEngine(n, cfg, dev)
         _ENGINES[key] = eng
-    eng.c_cfg = _lib.SkrConfig(cfg.m, cfg.k, cfg.max_iter, 0, cfg.tol)
+    eng.c_cfg = _lib.SkrConfig(cfg.m, cfg.k, cfg.max_iter, int(grid_ctas), cfg.tol)
     eng.cfg = cfg
     return eng
 

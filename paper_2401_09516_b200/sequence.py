@@ -101,11 +101,12 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
                    cfg: SolverConfig, precond: str = "none", *, positions: Sequence[int] = None,
                    keep_x: str = "host", stream=None, recycle_first=None,
                    want_history: bool = False, chain: ChainState = None,
-                   engine_slot: int = 0) -> SequenceResult:
+                   engine_slot: int = 0, grid_ctas: int = 0) -> SequenceResult:
     """Solve ``systems[order[p]]`` for p in ``positions`` (default: all) as one
     recycling chain. ``systems`` is a sequence of (A, b) or a callable idx ->
     (A, b) (lazy generation for large configs). ``keep_x``: "host" (x copied
-    back per system), "device" (kept as CUDA tensors) or "none"."""
+    back per system), "device" (kept as CUDA tensors) or "none". ``grid_ctas``:
+    CTAs of the Arnoldi kernel (0 = whole GPU; see solve_chains)."""
     import torch
 
     _lib.require_cuda()
@@ -129,6 +130,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
     U_prev_ptr, ld_prev = None, 0
     if chain is not None and chain.engine is not None:
         eng, U_prev_ptr, ld_prev, k_prev = chain.engine, chain.U_ptr, chain.ld, chain.k
+        eng.c_cfg = _lib.SkrConfig(cfg.m, cfg.k, cfg.max_iter, int(grid_ctas), cfg.tol)
     elif recycle_first is not None and recycle_first.k > 0:
         from .gcrodr import _colmajor_device
 
@@ -139,7 +141,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
         dA, bt, nb = nxt
         res.h2d_bytes += nb
         if eng is None:
-            eng = engine_for(dA.n, cfg, slot=engine_slot)
+            eng = engine_for(dA.n, cfg, slot=engine_slot, grid_ctas=grid_ctas)
         # prefetch the next system while this one solves
         if i + 1 < len(res.order):
             nxt = _upload(get(res.order[i + 1]), jacobi, side)
@@ -183,20 +185,38 @@ def split_chunks(positions: Sequence[int], parts: int) -> list:
     return [positions[i: i + per] for i in range(0, len(positions), per)]
 
 
+def chain_grid_ctas(n_chains: int, sms: int = None) -> int:
+    """Per-chain CTA count of the Arnoldi kernel when ``n_chains`` chains share
+    one GPU: the chains' cooperative kernels then run side by side on disjoint
+    SM sets (each kernel's latency-bound phases - grid barriers, the serial LS
+    update, the single-CTA dense recycle update - overlap the other chains'
+    streaming sweeps). Measured on B200 at C1: 8 chains x 72 CTAs best."""
+    import torch
+
+    if n_chains <= 1:
+        return 0
+    if sms is None:
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return max(8, (4 * sms) // max(1, n_chains))
+
+
 def solve_chains(systems, order, cfg: SolverConfig, precond: str, chunks: Sequence,
-                 keep_x: str = "host", states: Sequence = None, want_history: bool = False):
+                 keep_x: str = "host", states: Sequence = None, want_history: bool = False,
+                 grid_ctas: int = None):
     """Run several independent recycling chains concurrently on one GPU, one
     host thread + CUDA stream + workspace each (the paper's chunked SKR,
     PAPER.md:2149-2184, applied inside a GPU). Each chunk is a contiguous run
-    of sorted positions; chain i continues from ``states[i]`` if given. With
-    SKR_FREE_SMS > 0 one chain's single-SM dense update overlaps the others'
-    Arnoldi cycles. Returns one SequenceResult per chunk."""
+    of sorted positions; chain i continues from ``states[i]`` if given.
+    ``grid_ctas``: CTAs per chain (None = chain_grid_ctas(len(chunks))).
+    Returns one SequenceResult per chunk."""
     import threading
 
     import torch
 
     _lib.require_cuda()
     dev = torch.cuda.current_device()
+    if grid_ctas is None:
+        grid_ctas = chain_grid_ctas(len(chunks))
     states = list(states) if states is not None else [None] * len(chunks)
     out = [None] * len(chunks)
     errs = []
@@ -208,7 +228,8 @@ def solve_chains(systems, order, cfg: SolverConfig, precond: str, chunks: Sequen
             with torch.cuda.stream(st):
                 out[i] = solve_sequence(systems, order, cfg, precond, positions=chunks[i],
                                         keep_x=keep_x, stream=st, chain=states[i],
-                                        engine_slot=i, want_history=want_history)
+                                        engine_slot=i, want_history=want_history,
+                                        grid_ctas=grid_ctas)
         except BaseException as e:  # surfaced below
             errs.append(e)
 

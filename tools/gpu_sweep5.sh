@@ -1,0 +1,13 @@
+timeout 300 python tools/prof_big.py 4 2 > gpurun_out/big4.log 2>&1; echo "C4 rc=$?"; tail -1 gpurun_out/big4.log | cut -c1-400
+run() {  # name, env..., args
+  name=$1; shift
+  env "$@" timeout 400 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e $BARGS > gpurun_out/bench_$name.log 2>&1; echo "$name rc=$?"
+  tail -1 gpurun_out/bench_$name.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', round(d['value'],2), 'it', round(d['iterations_mean'],1), 'split', d['time_split_ms'], 'us/step', round(d['us_per_arnoldi_step'],2), 'roof', d['roofline']['achieved'])" 2>&1 | tail -1
+}
+BARGS="--chains 8 --free-sms 0" run c8n36 SKR_NBLK=36
+BARGS="--chains 16 --free-sms 0" run c16n36 SKR_NBLK=36
+BARGS="--chains 8 --free-sms 0" run c8n48 SKR_NBLK=48
+BARGS="--chains 8 --free-sms 0" run c8n72 SKR_NBLK=72
+BARGS="--chains 16 --free-sms 0" run c16n24 SKR_NBLK=24
+BARGS="--chains 16 --free-sms 0" run c16n48 SKR_NBLK=48
+BARGS="--chains 4 --free-sms 0" run c4n72 SKR_NBLK=72

@@ -26,7 +26,8 @@ int skrh_eig(const double* A, int lda, int n, double* wr, double* wi) {
   Ctx c = ctx();
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) DA(h.a.M1, LDD, i, j) = DA(A, lda, i, j);
-  return eig_schur(c, h.a.M1, LDD, n, h.a.M3, LDD, wr, wi, h.a.vec + 2 * LDD, h.a.xwork);
+  return eig_schur(c, h.a.M1, LDD, n, h.a.M3, LDD, wr, wi, h.a.vec + 2 * LDD, h.a.M2,
+                   LDD * LDD / ZREC);
 }
 
 // eigen-decomposition with the selection: returns ncols, P (n x ncols) NOT
@@ -37,7 +38,8 @@ int skrh_select(const double* A, int lda, int n, int k, int max_cols, double* P,
   Ctx c = ctx();
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) DA(h.a.M1, LDD, i, j) = DA(A, lda, i, j);
-  if (eig_schur(c, h.a.M1, LDD, n, h.a.M3, LDD, wr, wi, h.a.vec + 2 * LDD, h.a.xwork) != 0)
+  if (eig_schur(c, h.a.M1, LDD, n, h.a.M3, LDD, wr, wi, h.a.vec + 2 * LDD, h.a.M2,
+                   LDD * LDD / ZREC) != 0)
     return -2;
   int nc = select_basis(c, h.a.M1, LDD, n, h.a.M3, LDD, wr, wi, k, max_cols, h.a.M4, LDD,
                         h.a.iw + LDD, h.a.xwork, h.a.red);

@@ -120,7 +120,9 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
   bsync();
   double* wr = ar.vec;
   double* wi = ar.vec + LDD;
-  if (eig_schur(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.xwork) != 0)
+  // Z log in M2 (the LU factors are dead; qrcp writes M2 only after select)
+  if (eig_schur(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.M2,
+                LDD * LDD / ZREC) != 0)
     return -D_QR_NOCONV;
   int ncols = select_basis(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, kk, m, ar.M4, LDD, ar.iw + LDD,
                            ar.xwork, ar.red);
@@ -194,7 +196,9 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
   double* wi = ar.vec + LDD;
   hessenberg(c, ar.M4, LDD, mm, ar.M3, LDD, ar.vec + 2 * LDD);
   SKR_PHASE(ar, c, 10, t0);
-  int est = hqr(c, ar.M4, LDD, mm, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.xwork);
+  // Z log in M1..M2 (adjacent; lhs and the LU factors are dead until select)
+  int est = hqr(c, ar.M4, LDD, mm, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.M1,
+                2 * LDD * LDD / ZREC);
   if (ar.prof && c.tid == 0) {
     ar.prof[7] += (long long)ar.vec[2 * LDD + 1];
     ar.prof[8] += (long long)ar.vec[2 * LDD + 2];

@@ -190,14 +190,16 @@ def chain_grid_ctas(n_chains: int, sms: int = None) -> int:
     one GPU: the chains' cooperative kernels then run side by side on disjoint
     SM sets (each kernel's latency-bound phases - grid barriers, the serial LS
     update, the single-CTA dense recycle update - overlap the other chains'
-    streaming sweeps). Measured on B200 at C1: 8 chains x 72 CTAs best."""
+    streaming sweeps). Measured on B200 at C1 (bench.py, 5 steps): 8 chains x
+    64 CTAs 130 systems/s; x 48: 108; x 74: 119; x 96: 110; 4 x 100: 73;
+    16 x 37: 95; one chain on the whole GPU: 24."""
     import torch
 
     if n_chains <= 1:
         return 0
     if sms is None:
         sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    return max(8, (4 * sms) // max(1, n_chains))
+    return max(8, (7 * sms) // (2 * max(1, n_chains)))
 
 
 def solve_chains(systems, order, cfg: SolverConfig, precond: str, chunks: Sequence,

@@ -134,3 +134,21 @@ def test_generators_match_reference_conventions():
     a = P.system_params(spec, 0)["a"]
     assert set(np.unique(a)) == {3.0, 12.0} and 0.2 < (a == 12).mean() < 0.8
     assert P.system_params(P.CONFIGS[2], 0)["params"].shape == (65537,)
+
+
+def test_chain_grid_ctas_share():
+    """Concurrent chains split the GPU: whole GPU for one chain, a share for
+    several (never below 8 CTAs)."""
+    from paper_2401_09516_b200.sequence import chain_grid_ctas
+
+    assert chain_grid_ctas(1, sms=148) == 0
+    assert chain_grid_ctas(8, sms=148) == 64
+    assert chain_grid_ctas(4, sms=148) == 129
+    assert chain_grid_ctas(200, sms=148) == 8
+
+
+def test_skr_config_has_grid_ctas():
+    from paper_2401_09516_b200 import _lib
+
+    names = [f[0] for f in _lib.SkrConfig._fields_]
+    assert names == ["m", "k", "max_iter", "grid_ctas", "tol"]

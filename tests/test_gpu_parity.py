@@ -255,3 +255,56 @@ def test_edge_cases():
     Z = skr.CsrMatrix(2, 2, [0, 1, 2], [1, 0], [1.0, 1.0])
     with pytest.raises(skr.ZeroPivotError):
         skr.build_preconditioner(Z, "jacobi")
+
+
+# ----------------------------------------------------------------------------- launch shapes
+@pytest.mark.parametrize("grid_ctas", [1, 2, 7, 0])
+def test_chain_grid_shapes(grid_ctas):
+    """The Arnoldi kernel's row tiling (1 or 2 rows per lane, several tiles per
+    warp, ragged last tile) does not change the chain: C1 reduced to 64^2 with
+    the kernel squeezed onto 1, 2 or 7 CTAs vs the oracle chain."""
+    skr = _skr()
+    from oracle import skr_oracle as orc
+
+    spec = _spec(1, n=64)
+    sy = [_system(spec, i) for i in range(3)]
+    cfg = skr.SolverConfig(m=40, k=10, tol=1e-8)
+    res = skr.solve_sequence([(A, b) for A, b, _ in sy], [0, 1, 2], cfg, "jacobi",
+                             grid_ctas=grid_ctas)
+    ops = [orc.Operator(A.row_ptr, A.col_idx, A.values, spec.N, True) for A, _, _ in sy]
+    ref = orc.chain(ops, [b for _, b, _ in sy], [0, 1, 2], orc.Cfg(m=40, k=10, tol=1e-8))
+    for pos in range(3):
+        assert res.converged[pos]
+        err = np.linalg.norm(res.x[pos] - ref[pos].x) / np.linalg.norm(ref[pos].x)
+        assert err < 1e-6, (grid_ctas, pos, err)
+        assert abs(res.iterations[pos] - ref[pos].iterations) <= 0.05 * ref[pos].iterations + 2
+
+
+def test_solve_chains_is_chunked_skr():
+    """solve_chains = independent cold-started chains over contiguous chunks of
+    the sorted order, run concurrently on one GPU."""
+    skr = _skr()
+    from oracle import skr_oracle as orc
+
+    g = _chain_fixture("darcy16")
+    cid, n, ns, m, k, jac = [int(v) for v in g["cfg"]]
+    spec = _spec(cid, n=n)
+    sy = [_system(spec, i) for i in range(ns)]
+    cfg = skr.SolverConfig(m=m, k=k, tol=1e-8, max_iter=20000)
+    order = list(g["order"])
+    chunks = skr.split_chunks(list(range(ns)), 3)
+    out = skr.solve_chains([(A, b) for A, b, _ in sy], order, cfg, "jacobi" if jac else "none",
+                           chunks, grid_ctas=2)
+    ocfg = orc.Cfg(m=m, k=k, tol=1e-8, max_iter=20000)
+    ops = [orc.Operator(A.row_ptr, A.col_idx, A.values, spec.N, bool(jac)) for A, _, _ in sy]
+    for ch, r in zip(chunks, out):
+        idxs = [order[p] for p in ch]
+        assert r.order == idxs
+        ref = orc.chain(ops, [b for _, b, _ in sy], idxs, ocfg)
+        it_ref = np.array([ref[i].iterations for i in idxs])
+        for j, i in enumerate(idxs):
+            assert r.converged[j]
+            err = np.linalg.norm(r.x[j] - ref[i].x) / np.linalg.norm(ref[i].x)
+            assert err < 1e-6, (i, err)
+        dev = np.abs(np.array(r.iterations) - it_ref) / it_ref
+        assert dev.mean() <= 0.05, dev

@@ -69,7 +69,8 @@ struct State {
   int iters, kc, kc_prev, k_new, converged, done, brk, ran, upd, j, cycles, defl_steps;
   int hist_len, nchecks, warn, status, abort_flag, zero_rhs, fallback, ncol_a, ncol_b, r_tmp,
       cm_mode, cm_nin_u, cm_nin_c, cm_nv, cm_nout_u, cm_nout_c, ncol_orig;
-  unsigned bar_count, bar_pad0[63];  // barrier words on separate 256-byte lines:
+  unsigned long long bar_count;      // barrier words on separate 256-byte lines:
+  unsigned bar_pad0[62];
   unsigned bar_gen, bar_pad1[63];    // pollers of bar_gen must not contend with arrivals
   int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(NT) k_final_resid(Ptrs p) {
 // combine: row-parallel small-coefficient update of U / C, in place
 // ---------------------------------------------------------------------------
 template <int KT>
-__global__ void __launch_bounds__(NT) k_combine(Ptrs p, int cycle_mode) {
+__global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
   State* st = p.st;
   if (cycle_mode) {
     if (!st->ran) return;
@@ -459,30 +460,51 @@ __global__ void __launch_bounds__(NT) k_combine(Ptrs p, int cycle_mode) {
       au[q] = 0.0;
       ac[q] = 0.0;
     }
+    // input columns in batches of 8 loads (issued before the FMAs)
+    constexpr int LB = KT >= 24 ? 4 : 8;
     if (nout_u > 0)
-      for (int c = 0; c < nin_u; ++c) {
-        double v = colU(p, c)[row];
+      for (int c0 = 0; c0 < nin_u; c0 += LB) {
+        double v[LB];
 #pragma unroll
-        for (int q = 0; q < KT; ++q)
-          if (q < nout_u) au[q] += v * s_cu[c + q * LDC];
-      }
-    if (nout_c > 0)
-      for (int c = 0; c < nin_c; ++c) {
-        double v = colC(p, cbase_in + c)[row];
+        for (int u = 0; u < LB; ++u) v[u] = c0 + u < nin_u ? colU(p, c0 + u)[row] : 0.0;
 #pragma unroll
-        for (int q = 0; q < KT; ++q)
-          if (q < nout_c) ac[q] += v * s_cc[c + q * LDC];
-      }
-    if (mode == CM_CYCLE && (nout_u > 0 || nout_c > 0)) {
-      for (int v = 0; v <= nv; ++v) {
-        double x = colV(p, v)[row];
-        if (v < nv)
+        for (int u = 0; u < LB; ++u) {
+          const int c = min(c0 + u, nin_u - 1);
 #pragma unroll
           for (int q = 0; q < KT; ++q)
-            if (q < nout_u) au[q] += x * s_cu[nin_u + v + q * LDC];
+            if (q < nout_u) au[q] += v[u] * s_cu[c + q * LDC];
+        }
+      }
+    if (nout_c > 0)
+      for (int c0 = 0; c0 < nin_c; c0 += LB) {
+        double v[LB];
 #pragma unroll
-        for (int q = 0; q < KT; ++q)
-          if (q < nout_c) ac[q] += x * s_cc[nin_c + v + q * LDC];
+        for (int u = 0; u < LB; ++u)
+          v[u] = c0 + u < nin_c ? colC(p, cbase_in + c0 + u)[row] : 0.0;
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int c = min(c0 + u, nin_c - 1);
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < nout_c) ac[q] += v[u] * s_cc[c + q * LDC];
+        }
+      }
+    if (mode == CM_CYCLE && (nout_u > 0 || nout_c > 0)) {
+      for (int v0 = 0; v0 <= nv; v0 += LB) {
+        double x[LB];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) x[u] = v0 + u <= nv ? colV(p, v0 + u)[row] : 0.0;
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int v = min(v0 + u, nv);
+          if (v < nv)
+#pragma unroll
+            for (int q = 0; q < KT; ++q)
+              if (q < nout_u) au[q] += x[u] * s_cu[nin_u + v + q * LDC];
+#pragma unroll
+          for (int q = 0; q < KT; ++q)
+            if (q < nout_c) ac[q] += x[u] * s_cc[nin_c + v + q * LDC];
+        }
       }
     }
 #pragma unroll
@@ -606,7 +628,7 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
 
 #define CYCLE_SYNC()                                              \
   do {                                                            \
-    if (!grid_sync(bc, bg, abt, nblk, &S.flag)) {                 \
+    if (!grid_sync(bc, bg, abt, nblk, &S.flag, gen_seen)) {       \
       if (tid == 0) {                                             \
         st->done = 1;                                             \
         if (blk == 0) flag_host(st, cycle_id, 1);                 \
@@ -686,8 +708,9 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     return csr_row(p.rp, p.ci, p.av, xv, row);
   };
   const size_t ld = p.ld;
-  unsigned* bc = &st->bar_count;
+  unsigned long long* bc = &st->bar_count;
   unsigned* bg = &st->bar_gen;
+  unsigned gen_seen = tid == 0 ? ld_relaxed_gpu(bg) : 0u;  // no barrier is in flight here
   int* abt = &st->abort_flag;
 
   // ---- cycle start --------------------------------------------------------
@@ -866,19 +889,24 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       if (t >= 1) {
         const int i = t - 1;
         double* hcol = S.hcol;
+        // the running entry stays in a register: one dependent FMA per rotation
+        double run = hcol[0];
+#pragma unroll 4
         for (int q = 0; q < i; ++q) {
-          double tt = S.cs[q] * hcol[q] + S.sn[q] * hcol[q + 1];
-          hcol[q + 1] = -S.sn[q] * hcol[q] + S.cs[q] * hcol[q + 1];
-          hcol[q] = tt;
+          const double cq = S.cs[q], sq = S.sn[q], nx = hcol[q + 1];
+          hcol[q] = fma(cq, run, sq * nx);
+          run = fma(-sq, run, cq * nx);
         }
-        double den = hypot(hcol[i], hcol[i + 1]);
+        hcol[i] = run;
+        double den = hypot(run, hcol[i + 1]);
         double cs_, sn_;
         if (den == 0.0) {
           cs_ = 1.0;
           sn_ = 0.0;
         } else {
-          cs_ = hcol[i] / den;
-          sn_ = hcol[i + 1] / den;
+          const double rd = 1.0 / den;
+          cs_ = run * rd;
+          sn_ = hcol[i + 1] * rd;
         }
         S.cs[i] = cs_;
         S.sn[i] = sn_;

@@ -37,11 +37,6 @@ __device__ __forceinline__ double csr_row(const int32_t* __restrict__ rp,
   return acc;
 }
 
-// Grid-wide barrier for a cooperatively launched kernel. Thread 0 of each CTA
-// arrives on a counter and spins (with backoff) on a generation word; the last
-// arriver resets the counter and bumps the generation. A spin longer than
-// BARRIER_TIMEOUT_NS sets *abort instead of hanging the GPU. Returns false
-// when the solve was aborted (uniform across the CTA).
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -59,33 +54,47 @@ __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-__device__ __forceinline__ bool grid_sync(unsigned* count, unsigned* gen, int* abort_flag,
-                                          unsigned nblk, int* s_flag) {
+// Grid-wide barrier for a cooperatively launched kernel. Thread 0 of each CTA
+// arrives on a 64-bit counter that is never reset (barrier b completes when it
+// reaches nblk * b: the arriver that makes it a multiple of nblk is the last)
+// and spins (with backoff) on a generation word that the last arriver bumps.
+// `gen_seen` is thread 0's copy of the generation (read once per launch with
+// ld_relaxed_gpu before the first barrier), so an uncontended barrier costs
+// one fence, one atomic round trip and the poll. A spin longer than
+// BARRIER_TIMEOUT_NS sets *abort and returns false (uniform across the CTA)
+// instead of hanging the GPU.
+__device__ __forceinline__ bool grid_sync(unsigned long long* count, unsigned* gen,
+                                          int* abort_flag, unsigned nblk, int* s_flag,
+                                          unsigned& gen_seen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned g = ld_relaxed_gpu(gen);
+    int aborted = 0;
     fence_acq_rel_gpu();  // release this CTA's writes (block-scope ordered by bar.sync)
-    unsigned arrived = atomicAdd(count, 1u);
-    if (arrived == nblk - 1) {
-      atomicExch(count, 0u);
+    const unsigned long long arrived = atomicAdd(count, 1ull) + 1ull;
+    if (arrived % nblk == 0) {
       fence_acq_rel_gpu();
       atomicAdd(gen, 1u);
     } else {
       unsigned long long t0 = gtimer();
       unsigned polls = 0;
-      while (ld_relaxed_gpu(gen) == g) {
+      while (ld_relaxed_gpu(gen) == gen_seen) {
         __nanosleep(polls < 64 ? 20 : 100);
         if ((++polls & 255) == 0) {
           if (gtimer() - t0 > BARRIER_TIMEOUT_NS) {
             atomicExch(abort_flag, 1);
+            aborted = 1;
             break;
           }
-          if (ld_relaxed_gpu(reinterpret_cast<unsigned*>(abort_flag))) break;
+          if (ld_relaxed_gpu(reinterpret_cast<unsigned*>(abort_flag))) {
+            aborted = 1;
+            break;
+          }
         }
       }
     }
+    gen_seen += 1u;
     fence_acq_rel_gpu();  // acquire the other CTAs' writes
-    *s_flag = (int)ld_relaxed_gpu(reinterpret_cast<unsigned*>(abort_flag));
+    *s_flag = aborted;
   }
   __syncthreads();
   return *s_flag == 0;

@@ -1,0 +1,9 @@
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
+for pf in 1 0; do
+  if [ $pf = 0 ]; then export SKR_NO_L2PF=1; fi
+  timeout 300 python tools/prof_big.py 4 2 > gpurun_out/big4_pf$pf.log 2>&1; echo "C4 pf=$pf rc=$?"; tail -1 gpurun_out/big4_pf$pf.log | cut -c150-400
+  timeout 400 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_pf$pf.log 2>&1; echo "bench pf=$pf rc=$?"
+  tail -1 gpurun_out/bench_pf$pf.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', round(d['value'],2), 'it', round(d['iterations_mean'],1), 'split', d['time_split_ms'], 'agg', round(d['roofline']['aggregate_gbs']))"
+done
+unset SKR_NO_L2PF
+timeout 300 python tools/prof_dense.py > gpurun_out/prof_dense.log 2>&1; echo "prof_dense rc=$?"; grep "cycle" gpurun_out/prof_dense.log

@@ -13,7 +13,8 @@ import threading
 from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_void_p
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libskr.so")
+# SKR_LIB_PATH: load another build (A/B measurements of older revisions)
+LIB_PATH = os.environ.get("SKR_LIB_PATH") or os.path.join(PKG, "libskr.so")
 
 EXPORTS = (
     "skr_version", "skr_status_string", "skr_device_info", "skr_spmv", "skr_residual",

@@ -190,6 +190,8 @@ __global__ void k_setup(State* st, int n, int ld, int m, int k, int max_iter, do
     st->jacobi = jacobi;
     st->nblk = nblk;
     st->rpb = rpb;
+    st->prof[30] = nblk;  // launch shape, reported by skr_gcrodr_profile
+    st->prof[31] = rpb;
     st->k_in = k_in;
     st->has_x0 = has_x0;
     st->host_flag = host_flag;
@@ -637,11 +639,25 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
     }                                                             \
   } while (0)
 
-constexpr int GT_COLS = KMAX * 2 + MMAX + 1;
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
-static_assert(GT_COLS * GT_LD >= NW * 2 * PVC, "sweep-1 partials alias the Gram tile");
-constexpr size_t CYCLE_DSMEM_FIXED =
-    sizeof(double) * (GT_COLS * GT_LD + MMAX * (MMAX + 1) / 2 + KMAX * MMAX);
+
+// k_cycle dynamic shared memory, sized by (m, kcap) (offsets in doubles):
+// [ Gram tile (2 kcap + m + 1 cols x GT_LD; aliased by the sweep-1 partials)
+//   | packed R (m (m+1)/2) | B (kcap x m) | optional CSR slice cache ]
+struct CycleSmemLayout {
+  size_t R, B, csr;
+};
+__host__ __device__ inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
+  CycleSmemLayout L;
+  size_t gt = (size_t)(2 * kcap + m + 1) * GT_LD;
+  if (gt < (size_t)NW * 2 * PVC) gt = (size_t)NW * 2 * PVC;
+  L.R = gt;
+  L.B = L.R + (size_t)m * (m + 1) / 2;
+  L.csr = (L.B + (size_t)kcap * m + 1) & ~(size_t)1;  // 16-byte aligned
+  return L;
+}
+// dynamic smem per CTA that keeps 2 CTAs (+ ~7.6 KB static each) on an SM
+constexpr size_t CYCLE_DSMEM_BUDGET = 96 * 1024;
 
 // R = rows per lane in the Arnoldi sweeps: warp-owned tiles of 32 R consecutive
 // rows; every lane keeps its rows' w = V_t and z = op(V_t) in registers.
@@ -650,11 +666,12 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   State* st = p.st;
   __shared__ CycleSmem S;
   extern __shared__ double cdyn[];
-  double* gtile = cdyn;                             // Gram tile, column-major, ld GT_LD
-  double* sacc = cdyn;  // aliases gtile (sweep 1 only): per-warp dot partials [a | bb], 2 PVC each
-  double* Rsm = cdyn + GT_COLS * GT_LD;             // packed R (Givens-rotated H)
-  double* Bsm = Rsm + MMAX * (MMAX + 1) / 2;        // B, ld KMAX
-  int* csr_rp = reinterpret_cast<int*>(Bsm + KMAX * MMAX);  // cached CSR slice (optional)
+  const CycleSmemLayout SL = cycle_smem_layout(st->m, p.kcap);
+  double* gtile = cdyn;        // Gram tile, column-major, ld GT_LD
+  double* sacc = cdyn;         // aliases gtile (sweep 1 only): per-warp partials [a | bb]
+  double* Rsm = cdyn + SL.R;   // packed R (Givens-rotated H)
+  double* Bsm = cdyn + SL.B;   // B, ld kcap
+  int* csr_rp = reinterpret_cast<int*>(cdyn + SL.csr);  // cached CSR slice (optional)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int blk = blockIdx.x, nblk = p.nblk;
   if (st->done) {
@@ -712,7 +729,6 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   unsigned* bg = &st->bar_gen;
   unsigned gen_seen = tid == 0 ? ld_relaxed_gpu(bg) : 0u;  // no barrier is in flight here
   int* abt = &st->abort_flag;
-
   // ---- cycle start --------------------------------------------------------
   if (defl) {
     reduce_partials(p.part, GRID_MAX, nblk, 0, 2 * kc, S.red);
@@ -815,6 +831,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
         if (!(lane & ((1 << SH) - 1)) && col < pb) sw[(idx / CB) * PVC + col] += tot;
       }
     }
+
     __syncthreads();
     // cross-CTA sums by fp64 red.add into a triple-buffered accumulator
     // (layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)); every CTA then
@@ -875,7 +892,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       for (int q = tid; q <= i + 1; q += NT) S.hcol[q] = (q <= i) ? S.hp[q] + A_[kc + q] : eta;
       for (int c = tid; c < kc; c += NT) {
         double v = S.bp[c] + A_[c];
-        Bsm[c + i * KMAX] = v;
+        Bsm[c + i * kcap] = v;
         if (blk == 0) st->B[c + i * LDB] = v;
       }
       if (blk == 0)
@@ -994,6 +1011,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
           if (!stop) Vn[rr] = zv / eta - tb[i] - vt * htt;
         }
       }
+
     }
     if (stop) {
       j = t;
@@ -1011,7 +1029,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
         }
         for (int c = lane; c < kc; c += 32) {
           double sacc = S.cr[c];
-          for (int q = 0; q < j; ++q) sacc -= Bsm[c + q * KMAX] * S.y[kc + q];
+          for (int q = 0; q < j; ++q) sacc -= Bsm[c + q * kcap] * S.y[kc + q];
           S.y[c] = sacc / S.dk[c];
         }
         __syncwarp();
@@ -1428,7 +1446,6 @@ __global__ void __launch_bounds__(NT) k_resid(int n, const int32_t* rp, const in
 // ---------------------------------------------------------------------------
 static size_t dense_smem_bytes() { return skrd::arena_doubles(NW) * sizeof(double); }
 
-constexpr size_t CSR_CAP_MAX = 32 * 1024;  // bytes of CSR slice cached per CTA
 
 struct DevInfo {
   int sms = 0;
@@ -1439,7 +1456,7 @@ struct DevInfo {
 static DevInfo g_dev[16];
 static std::mutex g_mu;
 
-// k_cycle instantiation for R rows per lane (1, 2, 4 or 8)
+// k_cycle instantiation for R rows per lane (1, 2 or 4)
 static const void* cycle_kernel(int R) {
   switch (R) {
     case 1: return (const void*)k_cycle<1>;
@@ -1478,13 +1495,15 @@ static int ensure_dev(DevInfo** out) {
     for (int v = 0; v < 3; ++v) {
       const void* f = cycle_kernel(1 << v);
       if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(CYCLE_DSMEM_FIXED + CSR_CAP_MAX)) != cudaSuccess)
+                               (int)CYCLE_DSMEM_BUDGET) != cudaSuccess)
         return SKR_ERR_CUDA;
       int nbv = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbv, f, NT,
-                                                        CYCLE_DSMEM_FIXED + CSR_CAP_MAX) != cudaSuccess)
+                                                        CYCLE_DSMEM_BUDGET) != cudaSuccess)
         return SKR_ERR_CUDA;
       nb = std::min(nb, nbv);
+      if (const char* e = getenv("SKR_CARVEOUT"))  // experiment: shared-memory carveout (%)
+        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     }
     d.cycle_blocks_per_sm = nb;
     const int combine_smem = 2 * LDC * KMAX * (int)sizeof(double);
@@ -1681,13 +1700,17 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const int k_eff = cfg->k == 0 ? 0 : k_in;
   // CSR slice cache: sized from the mean row length with headroom; CTAs whose
   // slice does not fit read the matrix from global memory instead.
+  const size_t cycle_fixed = cycle_smem_layout(cfg->m, L.kcap).csr * sizeof(double);
   size_t csr_cap = 0;
   {
     double per_row = (double)A->nnz / std::max(1, n);
-    size_t want = (size_t)((p.rpb + 1) * 4 + (per_row * p.rpb * 1.25 + 64) * 12 + 64);
-    if (want <= CSR_CAP_MAX && !getenv("SKR_NO_CSR_CACHE")) csr_cap = (want + 255) / 256 * 256;
+    size_t want = (size_t)((p.rpb + 1) * 4 + (per_row * p.rpb * 1.06 + 64) * 12 + 64);
+    want = (want + 255) / 256 * 256;
+    if (cycle_fixed + want <= CYCLE_DSMEM_BUDGET && !getenv("SKR_NO_CSR_CACHE")) csr_cap = want;
   }
-  size_t cycle_dsmem = CYCLE_DSMEM_FIXED + csr_cap;
+  size_t cycle_dsmem = cycle_fixed + csr_cap;
+  if (const char* e = getenv("SKR_SMEM_PAD"))  // experiment: extra dynamic smem per CTA
+    cycle_dsmem = std::min(CYCLE_DSMEM_BUDGET, cycle_dsmem + (size_t)atoi(e));
   int csr_cap_i = (int)csr_cap;
   const void* cycle_fn = cycle_kernel(cycle_rows_per_lane(p.rpb));
 

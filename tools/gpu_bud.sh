@@ -1,0 +1,6 @@
+big() { tag=$1; shift; env "$@" timeout 300 python tools/prof_big.py 4 2 > gpurun_out/bud4_$tag.log 2>&1; echo "C4 $tag rc=$?"; grep "grid" gpurun_out/bud4_$tag.log; tail -1 gpurun_out/bud4_$tag.log | cut -c230-400; }
+big cur
+big b66c SKR_LIB_PATH=$PWD/alt/b66c/libskr.so
+timeout 300 python tools/prof_big.py 3 1 > gpurun_out/bud3.log 2>&1; echo "C3 rc=$?"; grep grid gpurun_out/bud3.log; tail -1 gpurun_out/bud3.log | cut -c200-400
+timeout 400 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bud_b.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/bud_b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', round(d['value'],2), 'it', round(d['iterations_mean'],1), 'split', d['time_split_ms'], 'agg', round(d['roofline']['aggregate_gbs']))"

@@ -22,6 +22,10 @@ for i in range(nsys):
     systems.append((skr.CsrMatrix(spec.N, spec.N, rp, ci, v, validate=False), b))
 print(f"assembled {nsys} systems of N={spec.N} in {time.time() - t:.1f}s", flush=True)
 res = skr.solve_sequence(systems, list(range(nsys)), cfg, spec.precond, keep_x="none")
+_prof = np.zeros(32, dtype=np.int64)
+skr._lib.load().skr_gcrodr_profile(res.chain.engine.ws.data_ptr(), res.chain.engine.nbytes, spec.N,
+                                   cfg.m, cfg.k, _prof.ctypes.data)
+print("k_cycle grid", int(_prof[30]), "rows/CTA", int(_prof[31]), flush=True)
 peak = 6547.5
 gbs = res.spmv_ortho_bytes / (res.cycle_kernel_ms / 1e3) / 1e9
 out = {"config": cid, "N": spec.N, "iterations": res.iterations, "converged": res.converged,

@@ -134,6 +134,7 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
 }
 
 struct Ptrs {
+  int sm_R, sm_B, sm_csr;  // k_cycle dynamic smem offsets (doubles), cycle_smem_layout
   State* st;
   const int32_t* rp;
   const int32_t* ci;
@@ -647,7 +648,7 @@ constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-
 struct CycleSmemLayout {
   size_t R, B, csr;
 };
-__host__ __device__ inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
+inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
   CycleSmemLayout L;
   size_t gt = (size_t)(2 * kcap + m + 1) * GT_LD;
   if (gt < (size_t)NW * 2 * PVC) gt = (size_t)NW * 2 * PVC;
@@ -666,12 +667,12 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   State* st = p.st;
   __shared__ CycleSmem S;
   extern __shared__ double cdyn[];
-  const CycleSmemLayout SL = cycle_smem_layout(st->m, p.kcap);
-  double* gtile = cdyn;        // Gram tile, column-major, ld GT_LD
-  double* sacc = cdyn;         // aliases gtile (sweep 1 only): per-warp partials [a | bb]
-  double* Rsm = cdyn + SL.R;   // packed R (Givens-rotated H)
-  double* Bsm = cdyn + SL.B;   // B, ld kcap
-  int* csr_rp = reinterpret_cast<int*>(cdyn + SL.csr);  // cached CSR slice (optional)
+  // offsets from the host (cycle_smem_layout): kernel parameters, not registers
+  double* gtile = cdyn;          // Gram tile, column-major, ld GT_LD
+  double* sacc = cdyn;           // aliases gtile (sweep 1 only): per-warp partials [a | bb]
+  double* Rsm = cdyn + p.sm_R;   // packed R (Givens-rotated H)
+  double* Bsm = cdyn + p.sm_B;   // B, ld kcap
+  int* csr_rp = reinterpret_cast<int*>(cdyn + p.sm_csr);  // cached CSR slice (optional)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int blk = blockIdx.x, nblk = p.nblk;
   if (st->done) {
@@ -1700,7 +1701,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const int k_eff = cfg->k == 0 ? 0 : k_in;
   // CSR slice cache: sized from the mean row length with headroom; CTAs whose
   // slice does not fit read the matrix from global memory instead.
-  const size_t cycle_fixed = cycle_smem_layout(cfg->m, L.kcap).csr * sizeof(double);
+  const CycleSmemLayout SL = cycle_smem_layout(cfg->m, L.kcap);
+  p.sm_R = (int)SL.R;
+  p.sm_B = (int)SL.B;
+  p.sm_csr = (int)SL.csr;
+  const size_t cycle_fixed = SL.csr * sizeof(double);
   size_t csr_cap = 0;
   {
     double per_row = (double)A->nnz / std::max(1, n);

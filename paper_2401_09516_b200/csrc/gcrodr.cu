@@ -865,99 +865,106 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     ++red_idx;
     __syncthreads();
     // ---- LS / control (identical in every CTA) ------------------------------
+    // warp 0: eta, the final column t-1, its Givens update and the first-pass
+    // column t; warps 1..: copy the sweep-2 coefficients (a, and b unscaled:
+    // sweep 2 divides by eta). One block barrier.
+    static_assert(NW >= 2, "the LS phase splits warp 0 from the others");
     const double* A_ = S.red + 3;
     const double* BB = S.red + 3 + pb;
-    {
+    if (warp == 0) {
       double aa = 0.0, ab = 0.0, cc = 0.0;
-      for (int c = tid; c < pb; c += NT) {
+      for (int c = lane; c < pb; c += 32) {
         double av = (t >= 1) ? A_[c] : 0.0, bv = BB[c];
         aa += av * av;
         ab += av * bv;
         if (c < kc) cc += bv * bv;
       }
-      block_sum3(aa, ab, cc, S.bred);
-      if (tid == 0) {
-        double eta0 = (t >= 1) ? sqrt(fmax(S.red[0] - aa, 0.0)) : 1.0;
+      for (int o = 16; o > 0; o >>= 1) {
+        aa += __shfl_xor_sync(0xffffffffu, aa, o);
+        ab += __shfl_xor_sync(0xffffffffu, ab, o);
+        cc += __shfl_xor_sync(0xffffffffu, cc, o);
+      }
+      const double eta0 = (t >= 1) ? sqrt(fmax(S.red[0] - aa, 0.0)) : 1.0;
+      const bool brk0 =
+          t >= 1 && eta0 < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308);
+      if (t >= 1) {
+        // final column i = t-1: first pass + reorthogonalisation coefficients
+        const int i = t - 1;
+        for (int q = lane; q <= i + 1; q += 32) S.hcol[q] = (q <= i) ? S.hp[q] + A_[kc + q] : eta0;
+        for (int c = lane; c < kc; c += 32) {
+          double v = S.bp[c] + A_[c];
+          Bsm[c + i * kcap] = v;
+          if (blk == 0) st->B[c + i * LDB] = v;
+        }
+        if (blk == 0)
+          for (int q = lane; q < LDH; q += 32)
+            st->H[q + i * LDH] = (q <= i) ? S.hp[q] + A_[kc + q] : (q == i + 1 ? eta0 : 0.0);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        bool stop0 = false;
+        if (t >= 1) {
+          // Givens update of column i; the running entry stays in a register
+          const int i = t - 1;
+          double* hcol = S.hcol;
+          double run = hcol[0];
+#pragma unroll 4
+          for (int q = 0; q < i; ++q) {
+            const double cq = S.cs[q], sq = S.sn[q], nx = hcol[q + 1];
+            hcol[q] = fma(cq, run, sq * nx);
+            run = fma(-sq, run, cq * nx);
+          }
+          hcol[i] = run;
+          double den = hypot(run, hcol[i + 1]);
+          double cs_, sn_;
+          if (den == 0.0) {
+            cs_ = 1.0;
+            sn_ = 0.0;
+          } else {
+            const double rd = 1.0 / den;
+            cs_ = run * rd;
+            sn_ = hcol[i + 1] * rd;
+          }
+          S.cs[i] = cs_;
+          S.sn[i] = sn_;
+          hcol[i] = den;
+          S.gv[i + 1] = -sn_ * S.gv[i];
+          S.gv[i] = cs_ * S.gv[i];
+          hres = fabs(S.gv[i + 1]);
+          if (blk == 0) p.hist[st->hist_len + i] = hres;
+          stop0 = brk0 || hres <= abs_tol || t == s;
+        }
         S.sc[0] = eta0;
-        S.sc[4] = ab;
-        S.sc[5] = cc;
-        S.sc[2] = (t >= 1 && eta0 < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308)) ? 1.0 : 0.0;
+        S.sc[1] = stop0 ? 1.0 : 0.0;
+        S.sc[2] = brk0 ? 1.0 : 0.0;
+        if (!stop0) {
+          S.sc[3] = (S.red[1] - ab) / (eta0 * eta0);  // h_tt = (mu - a.bb) / eta^2
+          wn0_pending = sqrt(fmax(S.red[2] - cc, 0.0)) / eta0;
+        }
       }
-      __syncthreads();
-    }
-    const double eta = S.sc[0];
-    brk = S.sc[2] != 0.0;
-    if (t >= 1) {
-      // final column i = t-1: first pass + reorthogonalisation coefficients
-      const int i = t - 1;
-      for (int q = tid; q <= i + 1; q += NT) S.hcol[q] = (q <= i) ? S.hp[q] + A_[kc + q] : eta;
-      for (int c = tid; c < kc; c += NT) {
-        double v = S.bp[c] + A_[c];
-        Bsm[c + i * kcap] = v;
-        if (blk == 0) st->B[c + i * LDB] = v;
-      }
-      if (blk == 0)
-        for (int q = tid; q < LDH; q += NT)
-          st->H[q + i * LDH] = (q <= i) ? S.hp[q] + A_[kc + q] : (q == i + 1 ? eta : 0.0);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      // Givens update of column i (sequential); other threads scale in parallel
-      bool stop = false;
+      __syncwarp();
+      const bool stop0 = S.sc[1] != 0.0;
       if (t >= 1) {
         const int i = t - 1;
-        double* hcol = S.hcol;
-        // the running entry stays in a register: one dependent FMA per rotation
-        double run = hcol[0];
-#pragma unroll 4
-        for (int q = 0; q < i; ++q) {
-          const double cq = S.cs[q], sq = S.sn[q], nx = hcol[q + 1];
-          hcol[q] = fma(cq, run, sq * nx);
-          run = fma(-sq, run, cq * nx);
-        }
-        hcol[i] = run;
-        double den = hypot(run, hcol[i + 1]);
-        double cs_, sn_;
-        if (den == 0.0) {
-          cs_ = 1.0;
-          sn_ = 0.0;
-        } else {
-          const double rd = 1.0 / den;
-          cs_ = run * rd;
-          sn_ = hcol[i + 1] * rd;
-        }
-        S.cs[i] = cs_;
-        S.sn[i] = sn_;
-        hcol[i] = den;
-        S.gv[i + 1] = -sn_ * S.gv[i];
-        S.gv[i] = cs_ * S.gv[i];
-        hres = fabs(S.gv[i + 1]);
-        if (blk == 0) p.hist[st->hist_len + i] = hres;
-        stop = brk || hres <= abs_tol || t == s;
+        const int base = i * (i + 1) / 2;  // packed upper-triangular R
+        for (int q = lane; q <= i; q += 32) Rsm[base + q] = S.hcol[q];
       }
-      S.sc[1] = stop ? 1.0 : 0.0;
-      if (!stop) {
-        S.sc[3] = (S.red[1] - S.sc[4]) / (eta * eta);  // h_tt = (mu - a.bb) / eta^2
-        wn0_pending = sqrt(fmax(S.red[2] - S.sc[5], 0.0)) / eta;
+      if (!stop0) {  // first-pass column t (scaled), finalised at the next step
+        const double ie = 1.0 / eta0;
+        for (int c = lane; c < kc; c += 32) S.bp[c] = BB[c] * ie;
+        for (int q = lane; q < t; q += 32) S.hp[q] = BB[kc + q] * ie;
+        if (lane == 0) S.hp[t] = S.sc[3];
       }
     } else {
-      for (int c = tid - 1; c < pb; c += NT - 1) {
+      for (int c = tid - 32; c < pb; c += NT - 32) {
         S.a[c] = (t >= 1) ? A_[c] : 0.0;
-        S.bb[c] = BB[c] / eta;  // first-pass coefficients of the new column
+        S.bb[c] = BB[c];
       }
     }
     __syncthreads();
+    const double eta = S.sc[0];
+    brk = S.sc[2] != 0.0;
     const bool stop = S.sc[1] != 0.0;
-    if (t >= 1) {
-      const int i = t - 1;
-      const int base = i * (i + 1) / 2;  // packed upper-triangular R
-      for (int q = tid; q <= i; q += NT) Rsm[base + q] = S.hcol[q];
-    }
-    if (!stop) {
-      for (int c = tid; c < kc; c += NT) S.bp[c] = S.bb[c];
-      for (int q = tid; q < t; q += NT) S.hp[q] = S.bb[kc + q];
-      if (tid == 0) S.hp[t] = S.sc[3];
-    }
     CPROF(2);
     // ---- sweep 2: finish V_t, project the new vector into V_{t+1} ----------
     {
@@ -1009,7 +1016,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
             vt = brk ? 0.0 : (wv - ta[i]) / eta;
             Vt[rr] = vt;
           }
-          if (!stop) Vn[rr] = zv / eta - tb[i] - vt * htt;
+          if (!stop) Vn[rr] = (zv - tb[i]) / eta - vt * htt;  // tb: unscaled b
         }
       }
 

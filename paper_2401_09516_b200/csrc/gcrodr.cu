@@ -1510,8 +1510,6 @@ static int ensure_dev(DevInfo** out) {
                                                         CYCLE_DSMEM_BUDGET) != cudaSuccess)
         return SKR_ERR_CUDA;
       nb = std::min(nb, nbv);
-      if (const char* e = getenv("SKR_CARVEOUT"))  // experiment: shared-memory carveout (%)
-        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     }
     d.cycle_blocks_per_sm = nb;
     const int combine_smem = 2 * LDC * KMAX * (int)sizeof(double);
@@ -1721,8 +1719,6 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     if (cycle_fixed + want <= CYCLE_DSMEM_BUDGET && !getenv("SKR_NO_CSR_CACHE")) csr_cap = want;
   }
   size_t cycle_dsmem = cycle_fixed + csr_cap;
-  if (const char* e = getenv("SKR_SMEM_PAD"))  // experiment: extra dynamic smem per CTA
-    cycle_dsmem = std::min(CYCLE_DSMEM_BUDGET, cycle_dsmem + (size_t)atoi(e));
   int csr_cap_i = (int)csr_cap;
   const void* cycle_fn = cycle_kernel(cycle_rows_per_lane(p.rpb));
 

@@ -69,9 +69,9 @@ struct State {
   int iters, kc, kc_prev, k_new, converged, done, brk, ran, upd, j, cycles, defl_steps;
   int hist_len, nchecks, warn, status, abort_flag, zero_rhs, fallback, ncol_a, ncol_b, r_tmp,
       cm_mode, cm_nin_u, cm_nin_c, cm_nv, cm_nout_u, cm_nout_c, ncol_orig;
-  unsigned long long bar_count;      // barrier words on separate 256-byte lines:
-  unsigned bar_pad0[62];
-  unsigned bar_gen, bar_pad1[63];    // pollers of bar_gen must not contend with arrivals
+  unsigned long long bar_count;      // grid-barrier arrivals (never reset within a solve),
+  unsigned bar_pad0[62];             // alone on its 256-byte line
+  unsigned bar_pad1[64];
   int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
   int steps, pad2;    // Arnoldi steps executed
@@ -631,7 +631,7 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
 
 #define CYCLE_SYNC()                                              \
   do {                                                            \
-    if (!grid_sync(bc, bg, abt, nblk, &S.flag, gen_seen)) {       \
+    if (!grid_sync(bc, abt, nblk, &S.flag, bar_seen)) {           \
       if (tid == 0) {                                             \
         st->done = 1;                                             \
         if (blk == 0) flag_host(st, cycle_id, 1);                 \
@@ -727,8 +727,8 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   };
   const size_t ld = p.ld;
   unsigned long long* bc = &st->bar_count;
-  unsigned* bg = &st->bar_gen;
-  unsigned gen_seen = tid == 0 ? ld_relaxed_gpu(bg) : 0u;  // no barrier is in flight here
+  // completed grid barriers of this solve (no barrier is in flight at launch)
+  unsigned long long bar_seen = tid == 0 ? ld_relaxed_gpu64(bc) / (unsigned long long)nblk : 0ull;
   int* abt = &st->abort_flag;
   // ---- cycle start --------------------------------------------------------
   if (defl) {

@@ -55,29 +55,32 @@ __device__ __forceinline__ void fence_acq_rel_gpu() {
 }
 
 // Grid-wide barrier for a cooperatively launched kernel. Thread 0 of each CTA
-// arrives on a 64-bit counter that is never reset (barrier b completes when it
-// reaches nblk * b: the arriver that makes it a multiple of nblk is the last)
-// and spins (with backoff) on a generation word that the last arriver bumps.
-// `gen_seen` is thread 0's copy of the generation (read once per launch with
-// ld_relaxed_gpu before the first barrier), so an uncontended barrier costs
-// one fence, one atomic round trip and the poll. A spin longer than
+// arrives on a 64-bit counter that is never reset within a solve: barrier b
+// (counted from the start of the solve) is complete when the counter reaches
+// nblk * (b + 1), which every CTA polls for directly (no separate generation
+// word, so the last arriver does no extra round trip). `seen` is thread 0's
+// count of completed barriers (counter / nblk, read once per launch with
+// ld_relaxed_gpu64 while no barrier is in flight). A spin longer than
 // BARRIER_TIMEOUT_NS sets *abort and returns false (uniform across the CTA)
 // instead of hanging the GPU.
-__device__ __forceinline__ bool grid_sync(unsigned long long* count, unsigned* gen,
-                                          int* abort_flag, unsigned nblk, int* s_flag,
-                                          unsigned& gen_seen) {
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool grid_sync(unsigned long long* count, int* abort_flag, unsigned nblk,
+                                          int* s_flag, unsigned long long& seen) {
   __syncthreads();
   if (threadIdx.x == 0) {
     int aborted = 0;
+    const unsigned long long target = (seen + 1ull) * nblk;
     fence_acq_rel_gpu();  // release this CTA's writes (block-scope ordered by bar.sync)
     const unsigned long long arrived = atomicAdd(count, 1ull) + 1ull;
-    if (arrived % nblk == 0) {
-      fence_acq_rel_gpu();
-      atomicAdd(gen, 1u);
-    } else {
+    if (arrived < target) {
       unsigned long long t0 = gtimer();
       unsigned polls = 0;
-      while (ld_relaxed_gpu(gen) == gen_seen) {
+      while (ld_relaxed_gpu64(count) < target) {
         __nanosleep(polls < 64 ? 20 : 100);
         if ((++polls & 255) == 0) {
           if (gtimer() - t0 > BARRIER_TIMEOUT_NS) {
@@ -92,7 +95,7 @@ __device__ __forceinline__ bool grid_sync(unsigned long long* count, unsigned* g
         }
       }
     }
-    gen_seen += 1u;
+    seen += 1ull;
     fence_acq_rel_gpu();  // acquire the other CTAs' writes
     *s_flag = aborted;
   }

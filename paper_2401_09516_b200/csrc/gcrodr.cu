@@ -82,8 +82,6 @@ struct State {
   // acc[(b * PV_STEP + v) * ACC_STRIDE]: one value per 256-byte line so the
   // fp64 red.add traffic of all CTAs spreads over the L2 slices
   double acc[3 * PV_STEP * ACC_STRIDE];
-  // cross-Gram accumulators (entry e at gacc[e * ACC_STRIDE]); zero between uses
-  double gacc[MMAX * MMAX * ACC_STRIDE];
   // per-cycle small data
   double H[LDH * MMAX];
   double B[LDB * MMAX];
@@ -132,6 +130,9 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
   L.total = off;
   return L;
 }
+
+// p.part rows: [0, 16) per-cycle scalar partials, [16, 16 + mm^2) cross-Gram
+constexpr int GRAM_PART0 = 16;
 
 struct Ptrs {
   int sm_R, sm_B, sm_csr;  // k_cycle dynamic smem offsets (doubles), cycle_smem_layout
@@ -201,8 +202,6 @@ __global__ void k_setup(State* st, int n, int ld, int m, int k, int max_iter, do
       host_flag[1] = 0;
     }
   }
-  // cross-Gram accumulators must start at zero (k_cycle re-zeroes after use)
-  for (int e = threadIdx.x; e < MMAX * MMAX; e += blockDim.x) st->gacc[(size_t)e * ACC_STRIDE] = 0.0;
 }
 
 // x = x0 or 0; r = M^-1 (b - A x) or M^-1 b; partials: |b|^2, |M^-1 b|^2, |r|^2
@@ -833,26 +832,37 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       }
     }
 
+    // warp partials of |w|^2, w.z, |z|^2 next to the column partials
+    for (int o = 16; o > 0; o >>= 1) {
+      nu += __shfl_xor_sync(0xffffffffu, nu, o);
+      mu += __shfl_xor_sync(0xffffffffu, mu, o);
+      ze += __shfl_xor_sync(0xffffffffu, ze, o);
+    }
+    if (lane == 0) {
+      S.bred[3 * warp] = nu;
+      S.bred[3 * warp + 1] = mu;
+      S.bred[3 * warp + 2] = ze;
+    }
     __syncthreads();
     // cross-CTA sums by fp64 red.add into a triple-buffered accumulator
     // (layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)); every CTA then
     // reads the same totals. Buffer (r+2)%3 is zeroed after barrier r: its
     // last readers finished before they arrived there.
     double* accb = st->acc + (size_t)(red_idx % 3) * PV_STEP * ACC_STRIDE;
-    for (int e = tid; e < 2 * pb; e += NT) {
-      const int which = e >= pb, col = which ? e - pb : e;
+    for (int e = tid; e < 3 + 2 * pb; e += NT) {
       double sum = 0.0;
+      bool use;
+      if (e < 3) {
 #pragma unroll
-      for (int q = 0; q < NW; ++q) sum += sacc[q * 2 * PVC + which * PVC + col];
-      if (which ? do_spmv : (t >= 1)) red_add_f64(accb + (size_t)(3 + e) * ACC_STRIDE, sum);
-    }
-    block_sum3(nu, mu, ze, S.bred);
-    if (tid == 0) {
-      red_add_f64(accb, nu);
-      if (do_spmv) {
-        red_add_f64(accb + ACC_STRIDE, mu);
-        red_add_f64(accb + 2 * ACC_STRIDE, ze);
+        for (int q = 0; q < NW; ++q) sum += S.bred[3 * q + e];
+        use = e == 0 || do_spmv;
+      } else {
+        const int which = e - 3 >= pb, col = which ? e - 3 - pb : e - 3;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) sum += sacc[q * 2 * PVC + which * PVC + col];
+        use = which ? do_spmv : (t >= 1);
       }
+      if (use) red_add_f64(accb + (size_t)e * ACC_STRIDE, sum);
     }
     CPROF(0);
     CYCLE_SYNC();
@@ -1085,8 +1095,8 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     // thread owns entries (ai + x*na4, bi + y*nb2), x < 4, y < 2, so
     // consecutive lanes read consecutive columns of a 32-row tile staged
     // column-major with an odd leading dimension (conflict-free). Per-CTA sums
-    // go straight to the cross accumulators with fp64 red.add (one 256-byte
-    // line per entry).
+    // go to p.part[(GRAM_PART0 + entry) * GRID_MAX + blk]; after the barrier
+    // every entry is summed over the CTAs in a fixed order (deterministic).
     // staged columns: [U (kc) | C (kc) | V_0..V_{j-1}]
     const int ncs = 2 * kc + j;
     const int na4 = (mm + 3) / 4, nb2 = (mm + 1) / 2;
@@ -1112,15 +1122,35 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
         cb[u][y] = ((b < kc) ? b : 2 * kc + (b - kc)) * GT_LD;  // Vhat col: U or V
       }
     }
-    for (int t0 = r0; t0 < r1; t0 += 32) {
-      for (int e = tid; e < 32 * ncs; e += NT) {
-        int rrw = e % 32, c = e / 32;
-        int row = t0 + rrw;
-        const double* col = (c < kc) ? colU(p, c)
-                            : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc))
-                                           : colV(p, c - 2 * kc);
-        gtile[c * GT_LD + rrw] = row < r1 ? col[row] : 0.0;
+    // the next 32-row tile is loaded into registers while this one is reduced
+    // (the first GPF elements per thread: all of them when ncs <= 64)
+    constexpr int GPF = 8;
+    auto tile_src = [&](int e, int t0) -> double {
+      const int rrw = e & 31, c = e >> 5, row = t0 + rrw;
+      const double* col = (c < kc) ? colU(p, c)
+                          : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc))
+                                         : colV(p, c - 2 * kc);
+      return row < r1 ? col[row] : 0.0;
+    };
+    double pf[GPF];
+    auto load_tile = [&](int t0) {
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT;
+        if (e < 32 * ncs) pf[k] = tile_src(e, t0);
       }
+    };
+    if (r0 < r1) load_tile(r0);
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT;
+        if (e < 32 * ncs) gtile[(e >> 5) * GT_LD + (e & 31)] = pf[k];
+      }
+      for (int e = tid + GPF * NT; e < 32 * ncs; e += NT)
+        gtile[(e >> 5) * GT_LD + (e & 31)] = tile_src(e, t0);
+      __syncthreads();
+      if (t0 + 32 < r1) load_tile(t0 + 32);
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -1153,7 +1183,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
           for (int y = 0; y < 2; ++y) {
             int a = ai + x * na4, b = bi + y * nb2;
             if (a < mm && b < mm)
-              red_add_f64(st->gacc + (size_t)(a + b * mm) * ACC_STRIDE, gacc[u][x * 2 + y]);
+              p.part[(size_t)(GRAM_PART0 + a + b * mm) * GRID_MAX + blk] = gacc[u][x * 2 + y];
           }
       }
     }
@@ -1166,14 +1196,18 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   CYCLE_SYNC();
   CPROF(11);
   if (defl) {
-    // the cross accumulators are complete after the barrier; scale Vhat's U
-    // columns by dk (Vhat = [U diag(dk), V]) into st->cross, re-zero for next use
-    for (int e = blk * NT + tid; e < mm * mm; e += nblk * NT) {
-      int a = e % mm, b = e / mm;
-      double* g = st->gacc + (size_t)e * ACC_STRIDE;
-      double v = *g;
-      *g = 0.0;
-      st->cross[a + b * LDX] = (b < kc) ? v * st->dk[b] : v;
+    // one warp per cross entry: sum the CTAs' partials (lane-strided, then a
+    // butterfly: a fixed order), scale Vhat's U columns by dk (Vhat =
+    // [U diag(dk), V]) into st->cross
+    for (int e = blk * NW + warp; e < mm * mm; e += nblk * NW) {
+      const double* q = p.part + (size_t)(GRAM_PART0 + e) * GRID_MAX;
+      double v = 0.0;
+      for (int c = lane; c < nblk; c += 32) v += q[c];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        const int a = e % mm, b = e / mm;
+        st->cross[a + b * LDX] = (b < kc) ? v * st->dk[b] : v;
+      }
     }
   }
   if (blk == 0) {

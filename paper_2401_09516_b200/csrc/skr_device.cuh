@@ -58,7 +58,8 @@ __device__ __forceinline__ void fence_acq_rel_gpu() {
 // arrives on a 64-bit counter that is never reset within a solve: barrier b
 // (counted from the start of the solve) is complete when the counter reaches
 // nblk * (b + 1), which every CTA polls for directly (no separate generation
-// word, so the last arriver does no extra round trip). `seen` is thread 0's
+// word, so the last arriver does no extra round trip; a fire-and-forget
+// red.release arrival measured slower than fence + atomicAdd). `seen` is thread 0's
 // count of completed barriers (counter / nblk, read once per launch with
 // ld_relaxed_gpu64 while no barrier is in flight). A spin longer than
 // BARRIER_TIMEOUT_NS sets *abort and returns false (uniform across the CTA)

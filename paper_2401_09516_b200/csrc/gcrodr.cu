@@ -62,7 +62,8 @@ enum CombineMode {
 
 struct State {
   // config
-  int n, ld, m, k, kcap, max_iter, jacobi, nblk, rpb, k_in, has_x0, pad0;
+  int n, ld, m, k, kcap, max_iter, jacobi, nblk, rpb, k_in, has_x0,
+      comb_part;  // cycle-start partials: 0 = rows [0, 2kc) (k_project), 1 = COMB_PART0 rows
   double tol;
   // scalars
   double bnorm, bprec, abs_tol, rnorm, true_rel;
@@ -122,7 +123,7 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
   L.z = off;
   off = align_up(off + (size_t)L.ld * sizeof(double), 256);
   L.part = off;
-  off = align_up(off + (size_t)(PV_MAX + 16) * GRID_MAX * sizeof(double), 256);
+  off = align_up(off + (size_t)(PV_MAX + 16 + 2 * KMAX) * GRID_MAX * sizeof(double), 256);
   L.hist = off;
   off = align_up(off + (size_t)L.hist_cap * sizeof(double), 256);
   L.checks = off;
@@ -131,8 +132,11 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
   return L;
 }
 
-// p.part rows: [0, 16) per-cycle scalar partials, [16, 16 + mm^2) cross-Gram
+// p.part rows: [0, 16) per-cycle scalar partials, [16, 16 + mm^2) cross-Gram,
+// [COMB_PART0, COMB_PART0 + 2 KMAX) next-cycle partials accumulated by k_combine
+// (fp64 red.add into slot blk % nblk; zeroed by k_init and after each read)
 constexpr int GRAM_PART0 = 16;
+constexpr int COMB_PART0 = GRAM_PART0 + PV_MAX;
 
 struct Ptrs {
   int sm_R, sm_B, sm_csr;  // k_cycle dynamic smem offsets (doubles), cycle_smem_layout
@@ -238,6 +242,8 @@ __global__ void __launch_bounds__(NT) k_init(Ptrs p, const double* x0) {
     p.part[1 * GRID_MAX + blockIdx.x] = t1;
     p.part[2 * GRID_MAX + blockIdx.x] = t2;
   }
+  for (int v = threadIdx.x; v < 2 * KMAX; v += NT)
+    p.part[(size_t)(COMB_PART0 + v) * GRID_MAX + blockIdx.x] = 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(NT) k_project(Ptrs p) {
   }
   double t = block_sum(rr, s_red);
   if (threadIdx.x == 0) p.part[(size_t)(2 * kc) * GRID_MAX + blockIdx.x] = t;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->comb_part = 0;
 }
 
 // true residual partials |b - A x|^2
@@ -452,7 +459,9 @@ __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
   for (int e = threadIdx.x; e < rows_c * nout_c; e += NT)
     s_cc[(e % rows_c) + (e / rows_c) * LDC] = cc[(e % rows_c) + (e / rows_c) * ldcc];
   __syncthreads();
-  int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  // own row split: the grid is not tied to the cooperative kernel's slices
+  const int rpc = (((p.n + gridDim.x - 1) / gridDim.x) + 31) & ~31;
+  int r0 = blockIdx.x * rpc, r1 = min(p.n, r0 + rpc);
   int cbase_in = p.kcap - nin_c;
   int cbase_out = p.kcap - nout_c;
   for (int row = r0 + threadIdx.x; row < r1; row += NT) {
@@ -518,6 +527,7 @@ __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
   if (mode == CM_CYCLE && !st->done) {
     // partials for the next cycle start: C^T r (kc) and |U_c|^2 (kc)
     int kc = st->kc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->comb_part = 1;
     __syncthreads();
     for (int c = 0; c < kc; ++c) {
       const double* C = colC(p, p.kcap - kc + c);
@@ -530,9 +540,10 @@ __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
       }
       double t1 = block_sum(s1, s_red);
       double t2 = block_sum(s2, s_red);
-      if (threadIdx.x == 0) {
-        p.part[(size_t)c * GRID_MAX + blockIdx.x] = t1;
-        p.part[(size_t)(kc + c) * GRID_MAX + blockIdx.x] = t2;
+      if (threadIdx.x == 0) {  // slot blk % nblk of the zeroed COMB_PART0 rows
+        const size_t slot = blockIdx.x % p.nblk;
+        red_add_f64(p.part + (size_t)(COMB_PART0 + c) * GRID_MAX + slot, t1);
+        red_add_f64(p.part + (size_t)(COMB_PART0 + kc + c) * GRID_MAX + slot, t2);
       }
     }
   }
@@ -730,8 +741,10 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   unsigned long long bar_seen = tid == 0 ? ld_relaxed_gpu64(bc) / (unsigned long long)nblk : 0ull;
   int* abt = &st->abort_flag;
   // ---- cycle start --------------------------------------------------------
+  const bool comb_part = st->comb_part != 0;
   if (defl) {
-    reduce_partials(p.part, GRID_MAX, nblk, 0, 2 * kc, S.red);
+    reduce_partials(p.part + (comb_part ? (size_t)COMB_PART0 * GRID_MAX : 0), GRID_MAX, nblk, 0,
+                    2 * kc, S.red);
     if (tid < kc) {
       double u2 = S.red[kc + tid];
       double un = sqrt(u2);
@@ -752,6 +765,9 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     for (int v = tid; v < 3 * PV_STEP; v += NT) st->acc[(size_t)v * ACC_STRIDE] = 0.0;
   int red_idx = 0;
   CYCLE_SYNC();
+  if (defl && comb_part && blk == 0)  // every CTA has read them: re-zero for k_combine
+    for (int e = tid; e < 2 * kc * nblk; e += NT)
+      p.part[(size_t)(COMB_PART0 + e / nblk) * GRID_MAX + e % nblk] = 0.0;
 
   int j = 0;
   bool brk = false;
@@ -925,15 +941,18 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
             run = fma(-sq, run, cq * nx);
           }
           hcol[i] = run;
-          double den = hypot(run, hcol[i + 1]);
-          double cs_, sn_;
-          if (den == 0.0) {
-            cs_ = 1.0;
-            sn_ = 0.0;
+          const double hn = hcol[i + 1];
+          const double d2 = fma(run, run, hn * hn);
+          double den, cs_, sn_;
+          if (d2 == 0.0 || !(d2 < 1e300) || d2 < 1e-300) {  // rare: the overflow-safe path
+            den = hypot(run, hn);
+            cs_ = den == 0.0 ? 1.0 : run / den;
+            sn_ = den == 0.0 ? 0.0 : hn / den;
           } else {
-            const double rd = 1.0 / den;
+            const double rd = rsqrt(d2);
+            den = d2 * rd;
             cs_ = run * rd;
-            sn_ = hcol[i + 1] * rd;
+            sn_ = hn * rd;
           }
           S.cs[i] = cs_;
           S.sn[i] = sn_;
@@ -948,8 +967,9 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
         S.sc[1] = stop0 ? 1.0 : 0.0;
         S.sc[2] = brk0 ? 1.0 : 0.0;
         if (!stop0) {
-          S.sc[3] = (S.red[1] - ab) / (eta0 * eta0);  // h_tt = (mu - a.bb) / eta^2
-          wn0_pending = sqrt(fmax(S.red[2] - cc, 0.0)) / eta0;
+          const double ie = 1.0 / eta0;
+          S.sc[3] = (S.red[1] - ab) * ie * ie;  // h_tt = (mu - a.bb) / eta^2
+          wn0_pending = sqrt(fmax(S.red[2] - cc, 0.0)) * ie;
         }
       }
       __syncwarp();
@@ -1755,6 +1775,10 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   size_t cycle_dsmem = cycle_fixed + csr_cap;
   int csr_cap_i = (int)csr_cap;
   const void* cycle_fn = cycle_kernel(cycle_rows_per_lane(p.rpb));
+  // k_combine is latency-bound per row: run it on >= 2 CTAs per SM (its
+  // next-cycle partials are folded into nblk slots, so the grid is free)
+  const int ncomb = std::max(1, std::min(std::min(GRID_MAX, std::max(nblk, 2 * d->sms)),
+                                         (n + 31) / 32));
 
   int* hflag = nullptr;
   int* dflag = nullptr;
@@ -1781,21 +1805,21 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
     k_reduce<<<8, NT, 0, s>>>(p, 0, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 0, -1);
-    launch_combine(kt, p, nblk, 0, s);
+    launch_combine(kt, p, ncomb, 0, s);
     k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
     k_reduce<<<8, NT, 0, s>>>(p, 0, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL2, 0, -1);
-    launch_combine(kt, p, nblk, 0, s);
+    launch_combine(kt, p, ncomb, 0, s);
     // W = op(Yo) into the C block; QRCP(W) -> C, U
     k_spmm<<<nblk, NT, 0, s>>>(p);
     k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
     k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 1, -1);
-    launch_combine(kt, p, nblk, 0, s);
+    launch_combine(kt, p, ncomb, 0, s);
     k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
     k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL2, 1, -1);
-    launch_combine(kt, p, nblk, 0, s);
+    launch_combine(kt, p, ncomb, 0, s);
     // projection alpha = C^T r ; x += U alpha ; r -= C alpha
     k_ctr<<<nblk, NT, 0, s>>>(p);
     k_reduce<<<8, NT, 0, s>>>(p, 2, 0);
@@ -1832,7 +1856,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
       cudaEventRecord(t_events.get(3 + 3 * (size_t)enq), s);
       k_dense<<<1, NT, dsm, s>>>(p, P_CYCLE, 0, enq);
       cudaEventRecord(t_events.get(4 + 3 * (size_t)enq), s);
-      launch_combine(kt, p, nblk, 1, s);
+      launch_combine(kt, p, ncomb, 1, s);
       launches += 3;
       ++enq;
     }

@@ -57,6 +57,8 @@ def _args():
     ap.add_argument("--grid", type=int, default=None, help="override grid side (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sync-steps", action="store_true",
+                    help="time each stripe separately (L2 flush + barrier between stripes)")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     return ap.parse_args()
 
@@ -311,33 +313,53 @@ def run_skr(args):
     sub = S // NC          # systems per chain per step
     span = (W + K) * sub   # positions per chain (contiguous sub-chunk of this rank's chunk)
 
+    def solve(systems, chunks, states, keep_x):
+        if NC == 1:
+            return [skr.solve_sequence(systems, ident, cfg, spec.precond, positions=chunks[0],
+                                       keep_x=keep_x, chain=states[0])]
+        return skr.solve_chains(systems, ident, cfg, spec.precond, chunks, keep_x=keep_x,
+                                states=states, grid_ctas=gctas)
+
+    def stripes(a, b):  # positions of stripes [a, b) for every chain
+        return [list(range(c * span + a * sub, c * span + b * sub)) for c in range(NC)]
+
     def run_pass(systems, keep_x):
+        """W untimed warm-up stripes, then K timed stripes. Default: the K stripes
+        run back to back in one timed region (chains do not wait for each other
+        at stripe boundaries); --sync-steps times each stripe separately with an
+        L2 flush and a barrier in between."""
         states = [None] * NC
         per_step, stats = [], []
         u_at_timed = None
-        for st in range(W + K):
-            _flush_l2(flush)
-            barrier()
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            chunks = [list(range(c * span + st * sub, c * span + (st + 1) * sub))
-                      for c in range(NC)]
-            if NC == 1:
-                rl = [skr.solve_sequence(systems, ident, cfg, spec.precond, positions=chunks[0],
-                                         keep_x=keep_x, chain=states[0])]
-            else:
-                rl = skr.solve_chains(systems, ident, cfg, spec.precond, chunks, keep_x=keep_x,
-                                      states=states, grid_ctas=gctas)
-            ev1.record()
-            barrier()
-            states = [r.chain for r in rl]
-            if st == W - 1 and states[0] is not None and states[0].k > 0:
-                U, C, k, ld = states[0].engine.recycle_views()
-                u_at_timed = U.cpu().numpy()
-            if st >= W:
-                per_step.append(ev0.elapsed_time(ev1))
-                stats.extend(rl)
-        return per_step, stats, u_at_timed
+        if args.sync_steps:
+            for st in range(W + K):
+                _flush_l2(flush)
+                barrier()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                rl = solve(systems, stripes(st, st + 1), states, keep_x)
+                ev1.record()
+                barrier()
+                states = [r.chain for r in rl]
+                if st == W - 1 and states[0] is not None and states[0].k > 0:
+                    u_at_timed = states[0].engine.recycle_views()[0].cpu().numpy()
+                if st >= W:
+                    per_step.append(ev0.elapsed_time(ev1))
+                    stats.extend(rl)
+            return per_step, stats, u_at_timed
+        rl = solve(systems, stripes(0, W), states, keep_x)
+        states = [r.chain for r in rl]
+        if states[0] is not None and states[0].k > 0:
+            u_at_timed = states[0].engine.recycle_views()[0].cpu().numpy()
+        _flush_l2(flush)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        rl = solve(systems, stripes(W, W + K), states, keep_x)
+        ev1.record()
+        barrier()
+        t = ev0.elapsed_time(ev1)
+        return [t / K] * K, list(rl), u_at_timed
 
     clocks = _Clocks()
     clocks.start()
@@ -389,7 +411,14 @@ def run_skr(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator; DCT-sampled GRF, see DESIGN.md)",
         "config": dict(_config_dict(spec, S, world), chains_per_gpu=NC,
-                       ctas_per_chain=gctas),
+                       ctas_per_chain=gctas,
+                       l2=("flushed between steps (256 MiB write)" if args.sync_steps else
+                           "flushed (256 MiB write) before the timed region; inside it each "
+                           "stripe's working set (per chain ~39 MB basis + CSR, x8 chains) "
+                           "exceeds the 126 MB L2"),
+                       timing=("each step timed separately" if args.sync_steps else
+                               "K stripes back to back in one timed region (CUDA events, "
+                               "barrier + synchronize on both sides); ms_per_step = total / K")),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "method": ("sum of k_cycle algorithmic bytes / timed-region device time "

@@ -123,11 +123,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
 int skr_gcrodr_recycle_view(void* workspace, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
                             double** U, double** C, int32_t* k_out, int32_t* ld);
 
-/* Phase clock counters of the solves since the workspace was set up
- * (32 x int64: [0,16) dense kernel, csrc/recycle.h SKR_PHASE; [16,24) cycle
- * kernel CTA 0) -- profiling aid. */
+/* Phase clock counters of the last solve (32 x int64: [0,16) dense kernel,
+ * csrc/recycle.h SKR_PHASE; [16,24) cycle kernel CTA 0; [30] cycle-kernel
+ * grid size, [31] rows per CTA) -- profiling aid. */
 int skr_gcrodr_profile(void* workspace, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
-                       long long* out16);
+                       long long* out32);
 
 /* Greedy nearest-neighbour sort. params: n_sys x P row-major fp64 (device).
  * dist2 fills D2[i - row0][j] = ||p_i - p_j||^2 for i in [row0, row1), all j

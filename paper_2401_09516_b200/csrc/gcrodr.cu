@@ -1949,12 +1949,12 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
 }
 
 int skr_gcrodr_profile(void* ws, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
-                       long long* out16) {
-  if (!ws || !out16) return SKR_ERR_ARG;
+                       long long* out32) {
+  if (!ws || !out32) return SKR_ERR_ARG;
   (void)ws_bytes;
   Layout L = make_layout(n, m, k, 1);
   State* st = (State*)((char*)ws + L.state);
-  if (cudaMemcpy(out16, st->prof, 32 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cudaMemcpy(out32, st->prof, 32 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return SKR_ERR_CUDA;
   return SKR_OK;
 }

@@ -13,7 +13,6 @@ constexpr int NT = 256;              // threads per CTA (streaming kernels)
 constexpr int NW = NT / 32;          // warps per CTA
 constexpr int KMAX = 32;             // max recycle columns incl. pair widening (k+1)
 constexpr int MMAX = 64;             // max Arnoldi columns (m + 1)
-constexpr int QMAX = (KMAX + MMAX + NW - 1) / NW;  // basis columns per warp in the dot phase
 constexpr int GRID_MAX = 1184;       // max persistent CTAs (148 SMs x 8)
 constexpr int PV_STEP = 2 * (KMAX + MMAX) + 8;      // reduction values per Arnoldi step
 constexpr int PV_MAX = MMAX * MMAX;  // largest reduction (cross-Gram mm x mm)
@@ -102,52 +101,6 @@ __device__ __forceinline__ bool grid_sync(unsigned long long* count, int* abort_
   }
   __syncthreads();
   return *s_flag == 0;
-}
-
-// ---------------------------------------------------------------------------
-// TMA bulk copies (cp.async.bulk, global -> shared) completing on an mbarrier
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* mbar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(mbar)),
-      "r"(phase)
-      : "memory");
-}
-// bytes: multiple of 16; src/dst 16-byte aligned
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
-                                            uint64_t* mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(mbar))
-      : "memory");
-}
-// generic-proxy global writes (this CTA's, ordered by bar.sync) before async-proxy reads
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_shared() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Sum over CTAs of partial values part[v * pstride + b], b < nblk, for

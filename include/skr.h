@@ -123,6 +123,28 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
 int skr_gcrodr_recycle_view(void* workspace, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
                             double** U, double** C, int32_t* k_out, int32_t* ld);
 
+/* One linear system of a chain: device CSR, right-hand side, solution out. */
+typedef struct skr_system {
+  skr_csr A;
+  const double* b;
+  double* x;
+} skr_system;
+
+/* The chain loop (harness.py:233-260) for several independent chains at once,
+ * on one GPU: chain c solves systems[chain_first[c] .. chain_first[c+1]) in
+ * that order, each solve refreshing from the U its predecessor left in the
+ * chain's workspace workspaces[c] (ws_bytes each); one native host thread and
+ * CUDA stream per chain, no host round trip between systems. U_first[c]
+ * (n x k_first[c], leading dim ldu_first[c]; may be NULL / 0) seeds chain c
+ * (e.g. the chain state of a previous call: the workspace's own U block).
+ * reports[i] receives system i's report. The chains' cycle kernels use
+ * cfg->grid_ctas CTAs each. Returns the first failing status. */
+int skr_gcrodr_solve_chains(const skr_system* systems, const int32_t* chain_first,
+                            int32_t n_chains, const skr_config* cfg, void* const* workspaces,
+                            size_t ws_bytes, const double* const* U_first,
+                            const int32_t* ldu_first, const int32_t* k_first,
+                            skr_report* reports);
+
 /* Phase clock counters of the last solve (32 x int64: [0,16) dense kernel,
  * csrc/recycle.h SKR_PHASE; [16,24) cycle kernel CTA 0; [30] cycle-kernel
  * grid size, [31] rows per CTA) -- profiling aid. */

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SKR_LIB_PATH") or os.path.join(PKG, "libskr.so")
 EXPORTS = (
     "skr_version", "skr_status_string", "skr_device_info", "skr_spmv", "skr_residual",
     "skr_gcrodr_workspace_bytes", "skr_gcrodr_solve", "skr_gcrodr_recycle_view",
-    "skr_gcrodr_profile",
+    "skr_gcrodr_profile", "skr_gcrodr_solve_chains",
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
     "skr_greedy_sort", "skr_dense_hr_first", "skr_dense_hr_next",
 )
@@ -32,6 +32,10 @@ class SkrExtensionError(RuntimeError):
 class SkrCsr(ctypes.Structure):
     _fields_ = [("n", c_int32), ("nnz", c_int32), ("row_ptr", c_void_p),
                 ("col_idx", c_void_p), ("values", c_void_p), ("diag", c_void_p)]
+
+
+class SkrSystem(ctypes.Structure):
+    _fields_ = [("A", SkrCsr), ("b", c_void_p), ("x", c_void_p)]
 
 
 class SkrConfig(ctypes.Structure):
@@ -77,6 +81,8 @@ def _declare(L):
                                      POINTER(c_void_p), POINTER(c_int32), POINTER(c_int32)],
                                     c_int32),
         "skr_gcrodr_profile": ([P, c_size_t, c_int32, c_int32, c_int32, P], c_int32),
+        "skr_gcrodr_solve_chains": ([POINTER(SkrSystem), P, c_int32, POINTER(SkrConfig), P,
+                                     c_size_t, P, P, P, POINTER(SkrReport)], c_int32),
         "skr_sort_workspace_bytes": ([c_int32, c_int64], c_size_t),
         "skr_sort_binary_check": ([P, c_int32, c_int64, P, POINTER(c_int32), P, c_size_t, P],
                                   c_int32),

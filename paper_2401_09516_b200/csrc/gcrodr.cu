@@ -1276,7 +1276,7 @@ __global__ void __launch_bounds__(NT) k_dense(Ptrs p, int prog, int arg, int cyc
   __shared__ int s_iw[8 * skrd::LDD];
   __shared__ int s_kept[KMAX];
   skrd::Ctx c = skrd::ctx();
-  skrd::Arena ar = skrd::make_arena(dsm, s_iw, c.nw);
+  skrd::Arena ar = skrd::make_arena(dsm, s_iw, c.nw, skrd::arena_ld(st->m));
   const int tid = threadIdx.x;
   switch (prog) {
     case P_INIT: {
@@ -1353,7 +1353,7 @@ __global__ void __launch_bounds__(NT) k_dense(Ptrs p, int prog, int arg, int cyc
       double* Rinv = ar.M4;
       // pass 2 on the materialised X1 (its Gram reduced into st->gram)
       int r2 = skrd::cholqr_pass2(c, ar, st->gram, LDK, r, st->R1, LDK, korig, T2, LDC, s_kept,
-                                  Rinv, skrd::LDD);
+                                  Rinv, ar.ld);
       if (arg == 1 && r2 > 0) {
         // U = Yo[:, kept] R'^-1 : coefU (ncol_a x r2), rows = Yo columns
         int ry = st->ncol_a;
@@ -1361,7 +1361,7 @@ __global__ void __launch_bounds__(NT) k_dense(Ptrs p, int prog, int arg, int cyc
           int i = e % ry, q = e / ry;
           double sacc = 0.0;
           for (int t = 0; t <= q; ++t)
-            if (s_kept[t] == i) sacc += Rinv[t + q * skrd::LDD];
+            if (s_kept[t] == i) sacc += Rinv[t + q * ar.ld];
           st->coefU[i + q * LDC] = sacc;
         }
       }
@@ -1462,7 +1462,7 @@ __global__ void __launch_bounds__(NT) k_dense_hr(const double* H, int ldh, int m
   extern __shared__ double dsm[];
   __shared__ int s_iw[8 * skrd::LDD];
   skrd::Ctx c = skrd::ctx();
-  skrd::Arena ar = skrd::make_arena(dsm, s_iw, c.nw);
+  skrd::Arena ar = skrd::make_arena(dsm, s_iw, c.nw, skrd::LDD);
   int warn = 0;
   int r;
   if (H) {
@@ -1506,7 +1506,11 @@ __global__ void __launch_bounds__(NT) k_resid(int n, const int32_t* rp, const in
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static size_t dense_smem_bytes() { return skrd::arena_doubles(NW) * sizeof(double); }
+// k_dense dynamic smem for Arnoldi length m (the arena's ld follows m, so at
+// m = 40 it is ~80 KB and the kernel fits next to a cycle CTA on an SM)
+static size_t dense_smem_bytes(int m = skrd::DMAX - 1) {
+  return skrd::arena_doubles(NW, skrd::arena_ld(m)) * sizeof(double);
+}
 
 
 struct DevInfo {
@@ -1620,7 +1624,31 @@ struct EventPool {
     return ev[i];
   }
 };
-static thread_local EventPool t_events;
+// timing events per stream (reused across solves and host threads: creating
+// CUDA objects in a fresh host thread while other chains' kernels run can
+// stall for a long time)
+static std::mutex g_pool_mu;
+static std::vector<std::pair<cudaStream_t, EventPool*>> g_pools;
+static EventPool& event_pool(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto& e : g_pools)
+    if (e.first == s) return *e.second;
+  g_pools.emplace_back(s, new EventPool());
+  return *g_pools.back().second;
+}
+// the native chain driver's streams, created once and reused
+static std::vector<cudaStream_t> g_chain_streams[16];
+static int chain_streams(int dev, int n, std::vector<cudaStream_t>& out) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto& v = g_chain_streams[dev];
+  while ((int)v.size() < n) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return SKR_ERR_CUDA;
+    v.push_back(s);
+  }
+  out.assign(v.begin(), v.begin() + n);
+  return SKR_OK;
+}
 
 // CTAs of the row-partitioned kernels: enough for >= SKR_ROWS_MIN (256) rows
 // each, at most what is co-resident on the GPU; `grid_ctas` > 0 (skr_config)
@@ -1787,6 +1815,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   hflag[0] = -1;
   hflag[1] = 0;
 
+  EventPool& t_events = event_pool(s);
   cudaEvent_t ev0 = t_events.get(0), ev1 = t_events.get(1);
   int launches = 0;
   cudaEventRecord(ev0, s);
@@ -1797,7 +1826,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
                       (size_t)n * sizeof(double), k_eff, cudaMemcpyDeviceToDevice, s);
   }
   k_init<<<nblk, NT, 0, s>>>(p, x0);
-  const size_t dsm = dense_smem_bytes();
+  const size_t dsm = dense_smem_bytes(cfg->m);
   k_dense<<<1, NT, dsm, s>>>(p, P_INIT, 0, -1);
   launches += 3;
   if (k_eff > 0) {
@@ -1861,17 +1890,27 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
       ++enq;
     }
     if (result) break;
-    // wait for cycle `seen` to be processed (or done)
+    // wait for cycle `seen` to be processed (or done). The mapped flag is
+    // polled with a short sleep; the driver (cudaStreamQuery) is asked only
+    // every ~64 polls -- several chains' threads spinning on it contend for
+    // the driver lock that their kernel launches also need. The look-ahead
+    // keeps LOOK cycles queued, so the poll latency does not idle the GPU.
+    unsigned polls = 0;
     while (true) {
       if (vf[1]) break;
       if (vf[0] >= seen) break;
+      if ((++polls & 63) != 0) {
+        std::this_thread::sleep_for(std::chrono::microseconds(5));
+        continue;
+      }
       cudaError_t q = cudaStreamQuery(s);
       if (q == cudaSuccess) {
         // stream drained: either done (flag) or stalled; re-check
         if (vf[1] || vf[0] >= seen) break;
         // nothing pending and no progress flag: the state says done
         int hdone = 0;
-        cudaMemcpy(&hdone, &p.st->done, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaMemcpyAsync(&hdone, &p.st->done, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
         if (hdone) {
           vf[1] = 1;
           break;
@@ -1904,7 +1943,10 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   release_slot(slot);
   if (result) return result;
   std::vector<char> hbuf(offsetof(State, kept));
-  cudaMemcpy(hbuf.data(), p.st, offsetof(State, kept), cudaMemcpyDeviceToHost);
+  // stream-ordered reads (never the legacy default stream: other chains run
+  // concurrently on their own streams)
+  cudaMemcpyAsync(hbuf.data(), p.st, offsetof(State, kept), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
   const State& hs = *reinterpret_cast<const State*>(hbuf.data());
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
@@ -1940,11 +1982,91 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   rep->launches = launches;
   rep->arnoldi_steps = hs.steps;
   if (hist && hist_cap > 0)
-    cudaMemcpy(hist, p.hist, sizeof(double) * std::min(hist_cap, hs.hist_len),
-               cudaMemcpyDeviceToHost);
+    cudaMemcpyAsync(hist, p.hist, sizeof(double) * std::min(hist_cap, hs.hist_len),
+                    cudaMemcpyDeviceToHost, s);
   if (checks && checks_cap > 0)
-    cudaMemcpy(checks, p.checks, sizeof(double) * 2 * std::min(checks_cap, hs.nchecks),
-               cudaMemcpyDeviceToHost);
+    cudaMemcpyAsync(checks, p.checks, sizeof(double) * 2 * std::min(checks_cap, hs.nchecks),
+                    cudaMemcpyDeviceToHost, s);
+  if ((hist && hist_cap > 0) || (checks && checks_cap > 0)) cudaStreamSynchronize(s);
+  return SKR_OK;
+}
+
+int skr_gcrodr_solve_chains(const skr_system* systems, const int32_t* chain_first,
+                            int32_t n_chains, const skr_config* cfg, void* const* workspaces,
+                            size_t ws_bytes, const double* const* U_first,
+                            const int32_t* ldu_first, const int32_t* k_first,
+                            skr_report* reports) {
+  if (!systems || !chain_first || n_chains < 1 || !cfg || !workspaces || !reports)
+    return SKR_ERR_ARG;
+  for (int c = 0; c < n_chains; ++c)
+    if (chain_first[c + 1] < chain_first[c] || !workspaces[c]) return SKR_ERR_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SKR_ERR_CUDA;
+  if (dev < 0 || dev >= 16) return SKR_ERR_UNSUPPORTED;
+  DevInfo* dinfo;
+  if (int rc0 = ensure_dev(&dinfo)) return rc0;
+  std::vector<cudaStream_t> streams;
+  if (int rc0 = chain_streams(dev, n_chains, streams)) return rc0;
+  for (int c = 0; c < n_chains; ++c) {  // event pools up front, on this thread
+    EventPool& ep = event_pool(streams[c]);
+    ep.get(2 + 3 * 64);
+  }
+  std::vector<int> status(n_chains, SKR_OK);
+  auto run_chain = [&](int c) {
+    if (cudaSetDevice(dev) != cudaSuccess) {
+      status[c] = SKR_ERR_CUDA;
+      return;
+    }
+    cudaStream_t s = streams[c];
+    if (getenv("SKR_TRACE"))
+      fprintf(stderr, "trace chain %d start_us %lld\n", c,
+              (long long)std::chrono::duration_cast<std::chrono::microseconds>(
+                  std::chrono::steady_clock::now().time_since_epoch())
+                  .count());
+    const double* U = U_first ? U_first[c] : nullptr;
+    int ldu = ldu_first ? ldu_first[c] : 0;
+    int k = k_first ? k_first[c] : 0;
+    if (!U) k = 0;
+    static const bool trace = getenv("SKR_TRACE") != nullptr;
+    for (int i = chain_first[c]; i < chain_first[c + 1]; ++i) {
+      const skr_system& sy = systems[i];
+      const auto h0 = std::chrono::steady_clock::now();
+      int rc = skr_gcrodr_solve(&sy.A, sy.b, nullptr, sy.x, cfg, k > 0 ? U : nullptr, ldu, k,
+                                workspaces[c], ws_bytes, &reports[i], nullptr, 0, nullptr, 0, s);
+      if (trace) {
+        const auto h1 = std::chrono::steady_clock::now();
+        auto us = [](std::chrono::steady_clock::time_point t) {
+          return (long long)std::chrono::duration_cast<std::chrono::microseconds>(
+                     t.time_since_epoch()).count();
+        };
+        fprintf(stderr, "trace chain %d sys %d host_us %lld %lld device_ms %.3f its %d\n", c, i,
+                us(h0), us(h1), reports[i].device_ms, reports[i].iterations);
+      }
+      if (rc != SKR_OK) {
+        status[c] = rc;
+        break;
+      }
+      // the next system refreshes from the U this solve left in the workspace
+      if (cfg->k > 0 && !reports[i].zero_rhs) {
+        double* Uw = nullptr;
+        int32_t kw = 0, ldw = 0;
+        Layout L = make_layout(sy.A.n, cfg->m, cfg->k, cfg->max_iter);
+        Uw = (double*)((char*)workspaces[c] + L.basis);
+        kw = reports[i].k_out;
+        ldw = L.ld;
+        U = Uw;
+        ldu = ldw;
+        k = kw;
+      }
+    }
+    cudaStreamSynchronize(s);
+  };
+  std::vector<std::thread> th;
+  th.reserve(n_chains);
+  for (int c = 0; c < n_chains; ++c) th.emplace_back(run_chain, c);
+  for (auto& t : th) t.join();
+  for (int c = 0; c < n_chains; ++c)
+    if (status[c] != SKR_OK) return status[c];
   return SKR_OK;
 }
 

@@ -14,7 +14,9 @@ struct HostArena {
   std::vector<double> d;
   std::vector<int> i;
   Arena a;
-  HostArena() : d(arena_doubles(1), 0.0), i(arena_ints(), 0) { a = make_arena(d.data(), i.data(), 1); }
+  HostArena() : d(arena_doubles(1, LDD), 0.0), i(arena_ints(LDD), 0) {
+    a = make_arena(d.data(), i.data(), 1, LDD);
+  }
 };
 }  // namespace
 

@@ -17,15 +17,16 @@
 namespace skrd {
 
 struct Arena {
-  double* G;   // LDD x LDD
-  double* M1;  // LDD x LDD
-  double* M2;  // LDD x LDD
-  double* M3;  // LDD x LDD
-  double* M4;  // LDD x LDD
-  double* vec;    // 12 * LDD
+  int ld;      // leading dimension of the matrices (odd, >= m + 1; <= LDD)
+  double* G;   // ld x ld
+  double* M1;  // ld x ld
+  double* M2;  // ld x ld
+  double* M3;  // ld x ld (M3, M4 adjacent: hr_next solves 2 mm right-hand sides)
+  double* M4;  // ld x ld
+  double* vec;    // 12 * ld
   double* xwork;  // nw * 3 * DMAX
   double* red;    // 64
-  int* iw;        // 8 * LDD
+  int* iw;        // 8 * ld
   long long* prof;  // optional phase clocks (device profiling), may be null
 };
 
@@ -41,21 +42,25 @@ struct Arena {
     }                                                             \
   } while (0)
 
-SKR_HD size_t arena_doubles(int nw) {
-  return (size_t)5 * LDD * LDD + 12 * LDD + (size_t)nw * 3 * DMAX + 64;
+// arena leading dimension for Arnoldi length m: the matrices are at most
+// (m + 1) x (m + 1); odd for fewer shared-memory bank conflicts
+SKR_HD int arena_ld(int m) { return (m + 1) | 1; }
+SKR_HD size_t arena_doubles(int nw, int ld) {
+  return (size_t)5 * ld * ld + 12 * ld + (size_t)nw * 3 * DMAX + 64;
 }
-SKR_HD size_t arena_ints() { return 8 * LDD; }
+SKR_HD size_t arena_ints(int ld) { return 8 * (size_t)ld; }
 
-SKR_HD Arena make_arena(double* d, int* iw, int nw) {
+SKR_HD Arena make_arena(double* d, int* iw, int nw, int ld) {
   Arena a;
-  size_t M = (size_t)LDD * LDD;
+  size_t M = (size_t)ld * ld;
+  a.ld = ld;
   a.G = d;
   a.M1 = d + M;
   a.M2 = d + 2 * M;
   a.M3 = d + 3 * M;
   a.M4 = d + 4 * M;
   a.vec = d + 5 * M;
-  a.xwork = a.vec + 12 * LDD;
+  a.xwork = a.vec + 12 * ld;
   a.red = a.xwork + (size_t)nw * 3 * DMAX;
   a.iw = iw;
   a.prof = 0;
@@ -64,10 +69,10 @@ SKR_HD Arena make_arena(double* d, int* iw, int nw) {
 
 // exact reference singularity test: sigma_max == 0 or sigma_min < 1e-14 sigma_max
 SKR_HD bool svd_singular(const Ctx& c, Arena& ar, const double* A, int lda, int n, double* work) {
-  copy_mat(c, A, lda, work, LDD, n, n);
+  copy_mat(c, A, lda, work, ar.ld, n, n);
   bsync();
-  double* sv = ar.vec + 8 * LDD;
-  jacobi_svd(c, work, LDD, n, n, 0, 0, sv, ar.red);
+  double* sv = ar.vec + 8 * ar.ld;
+  jacobi_svd(c, work, ar.ld, n, n, 0, 0, sv, ar.red);
   double mx = 0.0, mn = INFINITY;
   for (int i = 0; i < n; ++i) {
     mx = sv[i] > mx ? sv[i] : mx;
@@ -87,26 +92,26 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
   double hsub = DA(H, ldh, m, m - 1);
   for (Flat2 f_(c, m, m); f_.ok(); f_.next()) {
     int i = f_.i, j = f_.j;
-    DA(ar.M2, LDD, i, j) = DA(H, ldh, j, i);  // Hs^T
-    DA(ar.M1, LDD, i, j) = DA(H, ldh, i, j);  // Hs
+    DA(ar.M2, ar.ld, i, j) = DA(H, ldh, j, i);  // Hs^T
+    DA(ar.M1, ar.ld, i, j) = DA(H, ldh, i, j);  // Hs
   }
   bsync();
-  double fn = fro_norm(c, ar.M1, LDD, m, m, ar.red);
+  double fn = fro_norm(c, ar.M1, ar.ld, m, m, ar.red);
   int info = 0;
-  lu_factor(c, ar.M2, LDD, m, piv, &info);
+  lu_factor(c, ar.M2, ar.ld, m, piv, &info);
   bool singular = info != 0;
   if (!singular) {
     // [e_m | I]
     for (Flat2 f_(c, m, (m + 1)); f_.ok(); f_.next()) {
       int i = f_.i, j = f_.j;
-      DA(ar.M3, LDD, i, j) = (j == 0) ? (i == m - 1 ? 1.0 : 0.0) : (i == j - 1 ? 1.0 : 0.0);
+      DA(ar.M3, ar.ld, i, j) = (j == 0) ? (i == m - 1 ? 1.0 : 0.0) : (i == j - 1 ? 1.0 : 0.0);
     }
     bsync();
-    lu_solve(c, ar.M2, LDD, m, piv, ar.M3, LDD, m + 1);
-    double gn = fro_norm(c, ar.M3 + LDD, LDD, m, m, ar.red);
+    lu_solve(c, ar.M2, ar.ld, m, piv, ar.M3, ar.ld, m + 1);
+    double gn = fro_norm(c, ar.M3 + ar.ld, ar.ld, m, m, ar.red);
     if (!(fn * gn < KAPPA_CERT)) {
       *warn |= W_JACOBI_SVD;
-      singular = svd_singular(c, ar, ar.M1, LDD, m, ar.M4);
+      singular = svd_singular(c, ar, ar.M1, ar.ld, m, ar.M4);
     }
   }
   if (singular) {
@@ -116,20 +121,20 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
   }
   // modified = Hs + h^2 f e_m^T
   double h2 = hsub * hsub;
-  for (int i = c.tid; i < m; i += c.nt) DA(ar.M1, LDD, i, m - 1) += h2 * DA(ar.M3, LDD, i, 0);
+  for (int i = c.tid; i < m; i += c.nt) DA(ar.M1, ar.ld, i, m - 1) += h2 * DA(ar.M3, ar.ld, i, 0);
   bsync();
   double* wr = ar.vec;
-  double* wi = ar.vec + LDD;
+  double* wi = ar.vec + ar.ld;
   // Z log in M2 (the LU factors are dead; qrcp writes M2 only after select)
-  if (eig_schur(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.M2,
-                LDD * LDD / ZREC) != 0)
+  if (eig_schur(c, ar.M1, ar.ld, m, ar.M3, ar.ld, wr, wi, ar.vec + 2 * ar.ld, ar.M2,
+                ar.ld * ar.ld / ZREC) != 0)
     return -D_QR_NOCONV;
-  int ncols = select_basis(c, ar.M1, LDD, m, ar.M3, LDD, wr, wi, kk, m, ar.M4, LDD, ar.iw + LDD,
+  int ncols = select_basis(c, ar.M1, ar.ld, m, ar.M3, ar.ld, wr, wi, kk, m, ar.M4, ar.ld, ar.iw + ar.ld,
                            ar.xwork, ar.red);
   if (ncols < 0) return -D_LINALG_ERROR;
-  int* jp = ar.iw + 6 * LDD;
-  int r1 = qrcp(c, ar.M4, LDD, m, ncols, jp, ar.M2, LDD, RANK_RTOL, ar.vec + 2 * LDD,
-                ar.vec + 5 * LDD);
+  int* jp = ar.iw + 6 * ar.ld;
+  int r1 = qrcp(c, ar.M4, ar.ld, m, ncols, jp, ar.M2, ar.ld, RANK_RTOL, ar.vec + 2 * ar.ld,
+                ar.vec + 5 * ar.ld);
   return r1;
 }
 
@@ -140,41 +145,41 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
   int kk = k < mm ? k : mm;
   int* piv = ar.iw;
   long long t0 = SKR_CLK();
-  gemm(c, true, ar.G, LDD, ar.G, LDD, ar.M1, LDD, mm, mm, mm + 1);   // lhs = G^T G
-  gemm(c, true, ar.G, LDD, cross, ldx, ar.M2, LDD, mm, mm, mm);      // rhs = G[:mm]^T cross
+  gemm(c, true, ar.G, ar.ld, ar.G, ar.ld, ar.M1, ar.ld, mm, mm, mm + 1);   // lhs = G^T G
+  gemm(c, true, ar.G, ar.ld, cross, ldx, ar.M2, ar.ld, mm, mm, mm);      // rhs = G[:mm]^T cross
   bsync();
   SKR_PHASE(ar, c, 0, t0);
-  double fn = fro_norm(c, ar.M2, LDD, mm, mm, ar.red);
+  double fn = fro_norm(c, ar.M2, ar.ld, mm, mm, ar.red);
   int info = 0;
-  lu_factor(c, ar.M2, LDD, mm, piv, &info);
+  lu_factor(c, ar.M2, ar.ld, mm, piv, &info);
   bool singular = info != 0;
-  // one LU solve for [I | lhs]: I at M3 columns [LDD-mm, LDD), lhs at M4[:, 0:mm)
+  // one LU solve for [I | lhs]: I at M3 columns [ar.ld-mm, ar.ld), lhs at M4[:, 0:mm)
   // (M3 and M4 are adjacent, so the 2 mm right-hand sides are contiguous)
-  double* X = ar.M3 + (size_t)(LDD - mm) * LDD;
+  double* X = ar.M3 + (size_t)(ar.ld - mm) * ar.ld;
   if (!singular) {
     for (Flat2 f_(c, mm, mm); f_.ok(); f_.next()) {
       int i = f_.i, j = f_.j;
-      DA(X, LDD, i, j) = (i == j) ? 1.0 : 0.0;
-      DA(ar.M4, LDD, i, j) = DA(ar.M1, LDD, i, j);
+      DA(X, ar.ld, i, j) = (i == j) ? 1.0 : 0.0;
+      DA(ar.M4, ar.ld, i, j) = DA(ar.M1, ar.ld, i, j);
     }
     bsync();
-    lu_solve(c, ar.M2, LDD, mm, piv, X, LDD, 2 * mm);
-    double gn = fro_norm(c, X, LDD, mm, mm, ar.red);
+    lu_solve(c, ar.M2, ar.ld, mm, piv, X, ar.ld, 2 * mm);
+    double gn = fro_norm(c, X, ar.ld, mm, mm, ar.red);
     if (!(fn * gn < KAPPA_CERT)) {
       *warn |= W_JACOBI_SVD;
-      gemm(c, true, ar.G, LDD, cross, ldx, ar.M3, LDD, mm, mm, mm);  // rhs again
+      gemm(c, true, ar.G, ar.ld, cross, ldx, ar.M3, ar.ld, mm, mm, mm);  // rhs again
       bsync();
-      singular = svd_singular(c, ar, ar.M3, LDD, mm, ar.M2);
+      singular = svd_singular(c, ar, ar.M3, ar.ld, mm, ar.M2);
     }
   }
   SKR_PHASE(ar, c, 1, t0);
   if (singular) {
     *warn |= W_SINGULAR_CROSS;
     // pinv(rhs) via Jacobi SVD: M3 <- U S, M2 <- V, M4 <- pinv, A = pinv lhs -> M4
-    gemm(c, true, ar.G, LDD, cross, ldx, ar.M3, LDD, mm, mm, mm);
+    gemm(c, true, ar.G, ar.ld, cross, ldx, ar.M3, ar.ld, mm, mm, mm);
     bsync();
-    double* sv = ar.vec + 8 * LDD;
-    jacobi_svd(c, ar.M3, LDD, mm, mm, ar.M2, LDD, sv, ar.red);
+    double* sv = ar.vec + 8 * ar.ld;
+    jacobi_svd(c, ar.M3, ar.ld, mm, mm, ar.M2, ar.ld, sv, ar.red);
     double mx = 0.0;
     for (int i = 0; i < mm; ++i) mx = sv[i] > mx ? sv[i] : mx;
     double cut = 1e-15 * mx;  // numpy pinv default rcond
@@ -182,38 +187,38 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
       int i = f_.i, j = f_.j;
       double sacc = 0.0;
       for (int q = 0; q < mm; ++q)
-        if (sv[q] > cut) sacc += DA(ar.M2, LDD, i, q) * DA(ar.M3, LDD, j, q) / (sv[q] * sv[q]);
-      DA(ar.M4, LDD, i, j) = sacc;
+        if (sv[q] > cut) sacc += DA(ar.M2, ar.ld, i, q) * DA(ar.M3, ar.ld, j, q) / (sv[q] * sv[q]);
+      DA(ar.M4, ar.ld, i, j) = sacc;
     }
     bsync();
-    gemm(c, false, ar.M4, LDD, ar.M1, LDD, ar.M3, LDD, mm, mm, mm);  // pinv @ lhs
+    gemm(c, false, ar.M4, ar.ld, ar.M1, ar.ld, ar.M3, ar.ld, mm, mm, mm);  // pinv @ lhs
     bsync();
-    copy_mat(c, ar.M3, LDD, ar.M4, LDD, mm, mm);
+    copy_mat(c, ar.M3, ar.ld, ar.M4, ar.ld, mm, mm);
     bsync();
   }
   SKR_PHASE(ar, c, 2, t0);
   double* wr = ar.vec;
-  double* wi = ar.vec + LDD;
-  hessenberg(c, ar.M4, LDD, mm, ar.M3, LDD, ar.vec + 2 * LDD);
+  double* wi = ar.vec + ar.ld;
+  hessenberg(c, ar.M4, ar.ld, mm, ar.M3, ar.ld, ar.vec + 2 * ar.ld);
   SKR_PHASE(ar, c, 10, t0);
   // Z log in M1..M2 (adjacent; lhs and the LU factors are dead until select)
-  int est = hqr(c, ar.M4, LDD, mm, ar.M3, LDD, wr, wi, ar.vec + 2 * LDD, ar.M1,
-                2 * LDD * LDD / ZREC);
+  int est = hqr(c, ar.M4, ar.ld, mm, ar.M3, ar.ld, wr, wi, ar.vec + 2 * ar.ld, ar.M1,
+                2 * ar.ld * ar.ld / ZREC);
   if (ar.prof && c.tid == 0) {
-    ar.prof[7] += (long long)ar.vec[2 * LDD + 1];
-    ar.prof[8] += (long long)ar.vec[2 * LDD + 2];
+    ar.prof[7] += (long long)ar.vec[2 * ar.ld + 1];
+    ar.prof[8] += (long long)ar.vec[2 * ar.ld + 2];
     ar.prof[9] += 1;
-    for (int q = 0; q < 4; ++q) ar.prof[11 + q] += (long long)ar.vec[2 * LDD + 3 + q];
+    for (int q = 0; q < 4; ++q) ar.prof[11 + q] += (long long)ar.vec[2 * ar.ld + 3 + q];
   }
   SKR_PHASE(ar, c, 3, t0);
   if (est != 0) return -D_QR_NOCONV;
-  int ncols = select_basis(c, ar.M4, LDD, mm, ar.M3, LDD, wr, wi, kk, mm, ar.M1, LDD,
-                           ar.iw + LDD, ar.xwork, ar.red);
+  int ncols = select_basis(c, ar.M4, ar.ld, mm, ar.M3, ar.ld, wr, wi, kk, mm, ar.M1, ar.ld,
+                           ar.iw + ar.ld, ar.xwork, ar.red);
   SKR_PHASE(ar, c, 4, t0);
   if (ncols < 0) return -D_LINALG_ERROR;
-  int* jp = ar.iw + 6 * LDD;
-  int r1 = qrcp(c, ar.M1, LDD, mm, ncols, jp, ar.M2, LDD, RANK_RTOL, ar.vec + 2 * LDD,
-                ar.vec + 5 * LDD);
+  int* jp = ar.iw + 6 * ar.ld;
+  int r1 = qrcp(c, ar.M1, ar.ld, mm, ncols, jp, ar.M2, ar.ld, RANK_RTOL, ar.vec + 2 * ar.ld,
+                ar.vec + 5 * ar.ld);
   SKR_PHASE(ar, c, 5, t0);
   return r1;
 }
@@ -222,22 +227,22 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
 // Writes coefC (rows x r2) = Q and Zc (cols x r2) = Z. Returns r2.
 SKR_HD int gp_tail(const Ctx& c, Arena& ar, int rows, int cols, int r1, double* Zc, int ldz,
                    double* Qc, int ldq) {
-  gemm(c, false, ar.G, LDD, ar.M2, LDD, ar.M1, LDD, rows, r1, cols);
+  gemm(c, false, ar.G, ar.ld, ar.M2, ar.ld, ar.M1, ar.ld, rows, r1, cols);
   bsync();
-  int* jp = ar.iw + 6 * LDD;
-  int r2 = qrcp(c, ar.M1, LDD, rows, r1, jp, ar.M3, LDD, RANK_RTOL, ar.vec + 2 * LDD,
-                ar.vec + 5 * LDD);
+  int* jp = ar.iw + 6 * ar.ld;
+  int r2 = qrcp(c, ar.M1, ar.ld, rows, r1, jp, ar.M3, ar.ld, RANK_RTOL, ar.vec + 2 * ar.ld,
+                ar.vec + 5 * ar.ld);
   if (r2 <= 0) return 0;
-  inv_upper(c, ar.M1, LDD, r2, ar.M4, LDD);
+  inv_upper(c, ar.M1, ar.ld, r2, ar.M4, ar.ld);
   for (Flat2 f_(c, cols, r2); f_.ok(); f_.next()) {
     int i = f_.i, j = f_.j;
     double s = 0.0;
-    for (int q = 0; q <= j; ++q) s += DA(ar.M2, LDD, i, jp[q]) * DA(ar.M4, LDD, q, j);
+    for (int q = 0; q <= j; ++q) s += DA(ar.M2, ar.ld, i, jp[q]) * DA(ar.M4, ar.ld, q, j);
     DA(Zc, ldz, i, j) = s;
   }
   for (Flat2 f_(c, rows, r2); f_.ok(); f_.next()) {
     int i = f_.i, j = f_.j;
-    DA(Qc, ldq, i, j) = DA(ar.M3, LDD, i, j);
+    DA(Qc, ldq, i, j) = DA(ar.M3, ar.ld, i, j);
   }
   bsync();
   return r2;
@@ -253,7 +258,7 @@ SKR_HD int recycle_first(const Ctx& c, Arena& ar, const double* H, int ldh, int 
   if (r1 <= 0) return r1 < 0 ? r1 : 0;
   for (Flat2 f_(c, j + 1, j); f_.ok(); f_.next()) {
     int i = f_.i, q = f_.j;
-    DA(ar.G, LDD, i, q) = DA(H, ldh, i, q);
+    DA(ar.G, ar.ld, i, q) = DA(H, ldh, i, q);
   }
   bsync();
   return gp_tail(c, ar, j + 1, j, r1, coefU, ldu, coefC, ldcc);
@@ -266,7 +271,7 @@ SKR_HD int recycle_next(const Ctx& c, Arena& ar, const double* H, int ldh, const
                         int ldb, const double* dk, int kc, int j, const double* cross, int ldx,
                         int k, double* coefU, int ldu, double* coefC, int ldcc, int* warn) {
   int mm = kc + j;
-  if (mm + 1 > LDD) return -D_LINALG_ERROR;
+  if (mm + 1 > ar.ld) return -D_LINALG_ERROR;
   for (Flat2 f_(c, mm + 1, mm); f_.ok(); f_.next()) {
     int i = f_.i, q = f_.j;
     double v = 0.0;
@@ -276,7 +281,7 @@ SKR_HD int recycle_next(const Ctx& c, Arena& ar, const double* H, int ldh, const
       v = DA(B, ldb, i, q - kc);
     else if (q >= kc)
       v = DA(H, ldh, i - kc, q - kc);
-    DA(ar.G, LDD, i, q) = v;
+    DA(ar.G, ar.ld, i, q) = v;
   }
   bsync();
   int r1 = hr_next(c, ar, mm, cross, ldx, k, warn);
@@ -307,7 +312,7 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
   double* R = ar.M2;
   double* dsq = ar.vec;       // sqrt(diag)
   int* perm = ar.iw;          // k
-  int* meta = ar.iw + LDD;    // [0] = rank, [1] = pivot
+  int* meta = ar.iw + ar.ld;    // [0] = rank, [1] = pivot
   const double drop_tol = 1e-13;
   for (int i = c.tid; i < k; i += c.nt) {
     double d = DA(Gm, ldg, i, i);
@@ -318,18 +323,18 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
   for (Flat2 f_(c, k, k); f_.ok(); f_.next()) {
     int i = f_.i, j = f_.j;
     double den = dsq[i] * dsq[j];
-    DA(S, LDD, i, j) = den > 0.0 ? DA(Gm, ldg, i, j) / den : 0.0;
-    DA(R, LDD, i, j) = 0.0;
+    DA(S, ar.ld, i, j) = den > 0.0 ? DA(Gm, ldg, i, j) / den : 0.0;
+    DA(R, ar.ld, i, j) = 0.0;
   }
   bsync();
   int rank = k;
   for (int i = 0; i < k; ++i) {
     if (c.tid == 0) {
       int p = i;
-      double best = DA(S, LDD, i, i);
+      double best = DA(S, ar.ld, i, i);
       for (int q = i + 1; q < k; ++q)
-        if (DA(S, LDD, q, q) > best) {
-          best = DA(S, LDD, q, q);
+        if (DA(S, ar.ld, q, q) > best) {
+          best = DA(S, ar.ld, q, q);
           p = q;
         }
       meta[1] = p;
@@ -344,19 +349,19 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
     if (p != i) {
       // symmetric swap of rows/cols i,p of S, columns of R (rows < i), perm
       for (int q = c.tid; q < k; q += c.nt) {
-        double t = DA(S, LDD, i, q);
-        DA(S, LDD, i, q) = DA(S, LDD, p, q);
-        DA(S, LDD, p, q) = t;
+        double t = DA(S, ar.ld, i, q);
+        DA(S, ar.ld, i, q) = DA(S, ar.ld, p, q);
+        DA(S, ar.ld, p, q) = t;
       }
       bsync();
       for (int q = c.tid; q < k; q += c.nt) {
-        double t = DA(S, LDD, q, i);
-        DA(S, LDD, q, i) = DA(S, LDD, q, p);
-        DA(S, LDD, q, p) = t;
+        double t = DA(S, ar.ld, q, i);
+        DA(S, ar.ld, q, i) = DA(S, ar.ld, q, p);
+        DA(S, ar.ld, q, p) = t;
         if (q < i) {
-          double u = DA(R, LDD, q, i);
-          DA(R, LDD, q, i) = DA(R, LDD, q, p);
-          DA(R, LDD, q, p) = u;
+          double u = DA(R, ar.ld, q, i);
+          DA(R, ar.ld, q, i) = DA(R, ar.ld, q, p);
+          DA(R, ar.ld, q, p) = u;
         }
       }
       if (c.tid == 0) {
@@ -366,24 +371,24 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
       }
       bsync();
     }
-    double rii = sqrt(DA(S, LDD, i, i));
+    double rii = sqrt(DA(S, ar.ld, i, i));
     for (int q = i + c.tid; q < k; q += c.nt)
-      DA(R, LDD, i, q) = (q == i) ? rii : DA(S, LDD, i, q) / rii;
+      DA(R, ar.ld, i, q) = (q == i) ? rii : DA(S, ar.ld, i, q) / rii;
     bsync();
     int rem = k - i - 1;
     for (Flat2 f_(c, rem, rem); f_.ok(); f_.next()) {
       int a = i + 1 + f_.i, b = i + 1 + f_.j;
-      DA(S, LDD, a, b) -= DA(R, LDD, i, a) * DA(R, LDD, i, b);
+      DA(S, ar.ld, a, b) -= DA(R, ar.ld, i, a) * DA(R, ar.ld, i, b);
     }
     bsync();
   }
   // unscale: R_true(:, q) = R(:, q) * dsq[perm[q]]
   for (Flat2 f_(c, rank, k); f_.ok(); f_.next()) {
     int i = f_.i, q = f_.j;
-    DA(R, LDD, i, q) *= dsq[perm[q]];
+    DA(R, ar.ld, i, q) *= dsq[perm[q]];
   }
   bsync();
-  if (rank > 0) inv_upper(c, R, LDD, rank, ar.M3, LDD);
+  if (rank > 0) inv_upper(c, R, ar.ld, rank, ar.M3, ar.ld);
   for (Flat2 f_(c, k, rank); f_.ok(); f_.next()) {
     int i = f_.i, q = f_.j;
     DA(T1, ldt, i, q) = 0.0;
@@ -391,11 +396,11 @@ SKR_HD int cholqr_pass1(const Ctx& c, Arena& ar, const double* Gm, int ldg, int 
   bsync();
   for (Flat2 f_(c, rank, rank); f_.ok(); f_.next()) {
     int i = f_.i, q = f_.j;
-    DA(T1, ldt, perm[i], q) = DA(ar.M3, LDD, i, q);
+    DA(T1, ldt, perm[i], q) = DA(ar.M3, ar.ld, i, q);
   }
   for (Flat2 f_(c, rank, k); f_.ok(); f_.next()) {
     int i = f_.i, q = f_.j;
-    DA(R1, ldr, i, perm[q]) = DA(R, LDD, i, q);
+    DA(R1, ldr, i, perm[q]) = DA(R, ar.ld, i, q);
   }
   bsync();
   return rank;
@@ -412,18 +417,18 @@ SKR_HD int cholqr_pass2(const Ctx& c, Arena& ar, const double* G2, int ldg, int 
   // pass-2 Cholesky (pivoted routine: G2 ~ I, so it keeps every column)
   double* T2a = ar.G;  // r x r2a
   double* R2 = ar.M4;  // r2a x r (original order)
-  int r2a = cholqr_pass1(c, ar, G2, ldg, r, T2a, LDD, R2, LDD);
+  int r2a = cholqr_pass1(c, ar, G2, ldg, r, T2a, ar.ld, R2, ar.ld);
   if (r2a <= 0) return 0;
   // R_tot = R2 R1 (r2a x k) -> M1
-  gemm(c, false, R2, LDD, R1, ldr, ar.M1, LDD, r2a, k, r);
+  gemm(c, false, R2, ar.ld, R1, ldr, ar.M1, ar.ld, r2a, k, r);
   bsync();
-  int* jp = ar.iw + 6 * LDD;
-  int r2 = qrcp(c, ar.M1, LDD, r2a, k, jp, ar.M3, LDD, RANK_RTOL, ar.vec + 2 * LDD,
-                ar.vec + 5 * LDD);
+  int* jp = ar.iw + 6 * ar.ld;
+  int r2 = qrcp(c, ar.M1, ar.ld, r2a, k, jp, ar.M3, ar.ld, RANK_RTOL, ar.vec + 2 * ar.ld,
+                ar.vec + 5 * ar.ld);
   if (r2 <= 0) return 0;
   // T2 = T2a Q'[:, :r2]  (r x r2)
-  gemm(c, false, T2a, LDD, ar.M3, LDD, T2, ldt, r, r2, r2a);
-  inv_upper(c, ar.M1, LDD, r2, Rinv, ldri);
+  gemm(c, false, T2a, ar.ld, ar.M3, ar.ld, T2, ldt, r, r2, r2a);
+  inv_upper(c, ar.M1, ar.ld, r2, Rinv, ldri);
   for (int i = c.tid; i < r2; i += c.nt) kept[i] = jp[i];
   bsync();
   return r2;

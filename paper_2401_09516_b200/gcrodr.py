@@ -127,6 +127,14 @@ class GcroDrEngine:
     def u_block_ptr(self):
         return self.ws.data_ptr() + self._u_offset()
 
+    def u_ptr_ld(self):
+        """(device pointer of the U block, its leading dimension): fixed for the
+        workspace, so chains read them once (no device read per system)."""
+        if getattr(self, "_u_ptr_ld", None) is None:
+            _, _, _, ld = self.recycle_views()
+            self._u_ptr_ld = (self.u_block_ptr(), ld)
+        return self._u_ptr_ld
+
     def _u_offset(self):
         Up = ctypes.c_void_p()
         Cp = ctypes.c_void_p()

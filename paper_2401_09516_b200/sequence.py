@@ -16,6 +16,7 @@ sorted order) for the device engine, with three B200-first changes:
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
@@ -169,8 +170,9 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
             res.x.append(x)
         # chain: the next refresh reads U where this solve left it
         if cfg.k > 0 and not rep.zero_rhs:
-            U, C, k, ld = eng.recycle_views()
-            U_prev_ptr = U.data_ptr() if k else None
+            u_ptr, ld = eng.u_ptr_ld()
+            k = int(rep.k_out)
+            U_prev_ptr = u_ptr if k else None
             ld_prev, k_prev = ld, k
     torch.cuda.synchronize()
     res.wall_s = time.perf_counter() - t0
@@ -219,6 +221,11 @@ def solve_chains(systems, order, cfg: SolverConfig, precond: str, chunks: Sequen
     dev = torch.cuda.current_device()
     if grid_ctas is None:
         grid_ctas = chain_grid_ctas(len(chunks))
+    if keep_x in ("device", "none") and not want_history:
+        native = _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states,
+                                      grid_ctas)
+        if native is not None:
+            return native
     states = list(states) if states is not None else [None] * len(chunks)
     out = [None] * len(chunks)
     errs = []
@@ -242,4 +249,114 @@ def solve_chains(systems, order, cfg: SolverConfig, precond: str, chunks: Sequen
         t.join()
     if errs:
         raise errs[0]
+    return out
+
+
+def _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states, grid_ctas):
+    """solve_chains through skr_gcrodr_solve_chains: one native host thread and
+    stream per chain, no Python between systems. Only for device-resident
+    systems (DeviceCsr + CUDA b); returns None otherwise (the threaded path
+    then uploads host inputs per system)."""
+    import ctypes
+
+    import torch
+
+    t_enter = time.perf_counter()
+    get = systems if callable(systems) else (lambda i: systems[i])
+    jacobi = precond == "jacobi"
+    if precond not in ("none", "jacobi"):
+        raise NotImplementedError(f"preconditioner {precond!r} is not on the device path")
+    sysl, firsts, idxs = [], [0], []
+    for ch in chunks:
+        for pos in ch:
+            A, b = get(int(order[pos]))
+            if not (isinstance(A, DeviceCsr) and isinstance(b, torch.Tensor) and b.is_cuda):
+                return None
+            if jacobi and A.c.diag is None:
+                return None
+            sysl.append((A, b))
+            idxs.append(int(order[pos]))
+        firsts.append(len(sysl))
+    nch = len(chunks)
+    states = list(states) if states is not None else [None] * nch
+    n = sysl[0][0].n if sysl else 0
+    engines = []
+    for c in range(nch):
+        st = states[c]
+        if st is not None and st.engine is not None:
+            eng = st.engine
+            eng.c_cfg = _lib.SkrConfig(cfg.m, cfg.k, cfg.max_iter, int(grid_ctas), cfg.tol)
+        else:
+            eng = engine_for(n, cfg, slot=c, grid_ctas=grid_ctas)
+        engines.append(eng)
+    xs, arr = [], (_lib.SkrSystem * max(1, len(sysl)))()
+    dev = sysl[0][1].device if sysl else None
+    uniform = all(A.n == n for A, _ in sysl)
+    # outputs: one allocation for the whole call (views per system), or one
+    # scratch vector per chain when x is not kept
+    rows = len(sysl) if keep_x == "device" else nch
+    xbuf = torch.empty((rows, n), dtype=torch.float64, device=dev) if uniform and sysl else None
+    for c in range(nch):
+        for i in range(firsts[c], firsts[c + 1]):
+            A, b = sysl[i]
+            if xbuf is not None:
+                x = xbuf[i] if keep_x == "device" else xbuf[c]
+            else:
+                x = torch.empty(A.n, dtype=torch.float64, device=b.device)
+            xs.append(x)
+            arr[i].A = A.c
+            arr[i].b = b.data_ptr()
+            arr[i].x = x.data_ptr()
+    first_arr = (ctypes.c_int32 * (nch + 1))(*firsts)
+    ws_arr = (ctypes.c_void_p * nch)(*[e.ws.data_ptr() for e in engines])
+    u_arr = (ctypes.c_void_p * nch)()
+    ld_arr = (ctypes.c_int32 * nch)()
+    k_arr = (ctypes.c_int32 * nch)()
+    for c in range(nch):
+        st = states[c]
+        if st is not None and st.U_ptr is not None and st.k > 0:
+            u_arr[c], ld_arr[c], k_arr[c] = int(st.U_ptr), int(st.ld), int(st.k)
+    reps = (_lib.SkrReport * max(1, len(sysl)))()
+    nbytes = engines[0].nbytes if engines else 0
+    torch.cuda.synchronize()  # inputs ready on every stream
+    t0 = time.perf_counter()
+    L = _lib.load()
+    _lib.check(L.skr_gcrodr_solve_chains(arr, first_arr, nch, ctypes.byref(engines[0].c_cfg)
+                                         if engines else None, ws_arr, nbytes, u_arr, ld_arr,
+                                         k_arr, reps), "skr_gcrodr_solve_chains")
+    wall = time.perf_counter() - t0
+    t_native_end = time.perf_counter()
+    out = []
+    for c in range(nch):
+        res = SequenceResult(order=idxs[firsts[c]:firsts[c + 1]])
+        k_last, u_ptr, ld = 0, None, 0
+        for i in range(firsts[c], firsts[c + 1]):
+            rep = reps[i]
+            res.iterations.append(int(rep.iterations))
+            res.converged.append(bool(rep.converged))
+            res.true_rel.append(float(rep.true_relative_residual))
+            res.device_ms.append(float(rep.device_ms))
+            res.k_out.append(int(rep.k_out))
+            res.warn_bits.append(int(rep.warn_bits))
+            res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
+            res.launches += int(rep.launches)
+            res.cycle_kernel_ms += float(rep.cycle_kernel_ms)
+            res.dense_kernel_ms += float(rep.dense_kernel_ms)
+            res.arnoldi_steps += int(rep.arnoldi_steps)
+            if keep_x == "device":
+                res.x.append(xs[i])
+            if cfg.k > 0 and not rep.zero_rhs:
+                u_ptr, ld = engines[c].u_ptr_ld()
+                k_last = int(rep.k_out)
+        if firsts[c + 1] == firsts[c] and states[c] is not None:
+            res.chain = states[c]
+        else:
+            res.chain = ChainState(engines[c], u_ptr if k_last else None, ld, k_last)
+        res.wall_s = wall
+        out.append(res)
+    if os.environ.get("SKR_TRACE"):
+        import sys as _sys
+
+        print(f"trace py prep {1e3 * (t0 - t_enter):.2f} ms native {1e3 * wall:.2f} ms "
+              f"post {1e3 * (time.perf_counter() - t_native_end):.2f} ms", file=_sys.stderr)
     return out

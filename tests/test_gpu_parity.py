@@ -280,9 +280,12 @@ def test_chain_grid_shapes(grid_ctas):
         assert abs(res.iterations[pos] - ref[pos].iterations) <= 0.05 * ref[pos].iterations + 2
 
 
-def test_solve_chains_is_chunked_skr():
+@pytest.mark.parametrize("resident", [False, True])
+def test_solve_chains_is_chunked_skr(resident):
     """solve_chains = independent cold-started chains over contiguous chunks of
-    the sorted order, run concurrently on one GPU."""
+    the sorted order, run concurrently on one GPU: host
+    inputs through the threaded path, device-resident inputs through the
+    native skr_gcrodr_solve_chains driver."""
     skr = _skr()
     from oracle import skr_oracle as orc
 
@@ -293,8 +296,16 @@ def test_solve_chains_is_chunked_skr():
     cfg = skr.SolverConfig(m=m, k=k, tol=1e-8, max_iter=20000)
     order = list(g["order"])
     chunks = skr.split_chunks(list(range(ns)), 3)
-    out = skr.solve_chains([(A, b) for A, b, _ in sy], order, cfg, "jacobi" if jac else "none",
-                           chunks, grid_ctas=2)
+    if resident:
+        systems = [(skr.DeviceCsr.from_host(A, jacobi=bool(jac)), torch.from_numpy(b).cuda())
+                   for A, b, _ in sy]
+        out = skr.solve_chains(systems, order, cfg, "jacobi" if jac else "none", chunks,
+                               keep_x="device", grid_ctas=2)
+        for r in out:
+            r.x = [x.cpu().numpy() for x in r.x]
+    else:
+        out = skr.solve_chains([(A, b) for A, b, _ in sy], order, cfg,
+                               "jacobi" if jac else "none", chunks, grid_ctas=2)
     ocfg = orc.Cfg(m=m, k=k, tol=1e-8, max_iter=20000)
     ops = [orc.Operator(A.row_ptr, A.col_idx, A.values, spec.N, bool(jac)) for A, _, _ in sy]
     for ch, r in zip(chunks, out):

@@ -30,8 +30,8 @@ struct Arena {
   long long* prof;  // optional phase clocks (device profiling), may be null
 };
 
-// phase clock accumulation (thread 0 only): [0] products [1] LU + kappa
-// [2] solve [3] eig (Hessenberg + QR) [4] select + eigenvectors [5] QRCP(P)
+// phase clock accumulation (thread 0 only): [0] products [1] LU
+// [2] solve + kappa (+ the singular fallback) [3] eig (Hessenberg + QR) [4] select + eigenvectors [5] QRCP(P)
 // [6] GP tail [7] QR iterations [8] bulge steps [9] calls
 #define SKR_PHASE(ar, c, idx, t0)                                  \
   do {                                                            \
@@ -152,6 +152,7 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
   double fn = fro_norm(c, ar.M2, ar.ld, mm, mm, ar.red);
   int info = 0;
   lu_factor(c, ar.M2, ar.ld, mm, piv, &info);
+  SKR_PHASE(ar, c, 1, t0);
   bool singular = info != 0;
   // one LU solve for [I | lhs]: I at M3 columns [ar.ld-mm, ar.ld), lhs at M4[:, 0:mm)
   // (M3 and M4 are adjacent, so the 2 mm right-hand sides are contiguous)
@@ -172,7 +173,6 @@ SKR_HD int hr_next(const Ctx& c, Arena& ar, int mm, const double* cross, int ldx
       singular = svd_singular(c, ar, ar.M3, ar.ld, mm, ar.M2);
     }
   }
-  SKR_PHASE(ar, c, 1, t0);
   if (singular) {
     *warn |= W_SINGULAR_CROSS;
     // pinv(rhs) via Jacobi SVD: M3 <- U S, M2 <- V, M4 <- pinv, A = pinv lhs -> M4

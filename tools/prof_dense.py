@@ -22,7 +22,7 @@ L = _lib.load()
 prof = np.zeros(32, dtype=np.int64)
 L.skr_gcrodr_profile(eng.ws.data_ptr(), eng.nbytes, spec.N, cfg.m, cfg.k, prof.ctypes.data)
 calls = max(1, prof[9])
-names = ["products", "LU+kappa", "solve", "eig(hess+QR)", "select+eigvec", "qrcp(P)", "GP tail"]
+names = ["products", "LU", "solve+kappa", "eig(hess+QR)", "select+eigvec", "qrcp(P)", "GP tail"]
 print("iterations", res.iterations, "device_ms", [round(x, 2) for x in res.device_ms])
 print("cycle_ms", round(res.cycle_kernel_ms, 2), "dense_ms", round(res.dense_kernel_ms, 2),
       "steps", res.arnoldi_steps, "us/step", round(1000 * res.cycle_kernel_ms / res.arnoldi_steps, 2))

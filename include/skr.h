@@ -48,6 +48,13 @@ typedef struct skr_csr {
   const int32_t* col_idx;
   const double* values;
   const double* diag;
+  /* Optional symmetric 7-diagonal form of the same matrix (NULL = none),
+   * built by skr_stencil_build with diagonal offsets sx (and sxy, 0 in 2-D).
+   * Every kernel applying A uses it when the build verified that the CSR
+   * qualifies (results bit-identical to the CSR row sums), else the CSR. */
+  const void* stencil;
+  int32_t sx;
+  int32_t sxy;
 } skr_csr;
 
 /* SolverConfig (gmres.py:26-43) + one launch knob. */
@@ -106,6 +113,19 @@ int skr_spmv(const skr_csr* A, const double* x, double* y, int apply_prec, void*
 /* r = D^-1 (b - A x) (or b - A x): the reference's explicit residual. */
 int skr_residual(const skr_csr* A, const double* b, const double* x, double* r, int apply_prec,
                  void* stream);
+
+/* Stencil form of A (matrix-free 5-/7-point operator; replaces the CSR reads
+ * of sparse.py:155-160 csr_matvec on the hot path): the
+ * entries of a CSR whose pattern lies on the diagonals {0, +-1, +-sx, +-sxy}
+ * with bitwise-symmetric, nonzero off-diagonal values and a diagonal in every
+ * row are kept as D, W (-1), S (-sx), B (-sxy): 24 / 32 bytes per row instead
+ * of 64 / 88. skr_stencil_build verifies the pattern on the device
+ * (stream-ordered, no host sync); a matrix that does not qualify leaves the
+ * form disabled and the kernels fall back to the CSR. Returns 0 bytes for
+ * invalid offsets (sx >= 2, sxy == 0 or sxy > sx). */
+size_t skr_stencil_bytes(int32_t n, int32_t sx, int32_t sxy);
+int skr_stencil_build(const skr_csr* A, int32_t sx, int32_t sxy, void* buf, size_t bytes,
+                      void* stream);
 
 size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter);
 /* Solve A x = b with GCRO-DR. U_in (n x k_in, column-major, leading dim ldu)

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("SKR_LIB_PATH") or os.path.join(PKG, "libskr.so")
 
 EXPORTS = (
     "skr_version", "skr_status_string", "skr_device_info", "skr_spmv", "skr_residual",
+    "skr_stencil_bytes", "skr_stencil_build",
     "skr_gcrodr_workspace_bytes", "skr_gcrodr_solve", "skr_gcrodr_recycle_view",
     "skr_gcrodr_profile", "skr_gcrodr_solve_chains",
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
@@ -31,7 +32,8 @@ class SkrExtensionError(RuntimeError):
 
 class SkrCsr(ctypes.Structure):
     _fields_ = [("n", c_int32), ("nnz", c_int32), ("row_ptr", c_void_p),
-                ("col_idx", c_void_p), ("values", c_void_p), ("diag", c_void_p)]
+                ("col_idx", c_void_p), ("values", c_void_p), ("diag", c_void_p),
+                ("stencil", c_void_p), ("sx", c_int32), ("sxy", c_int32)]
 
 
 class SkrSystem(ctypes.Structure):
@@ -72,6 +74,8 @@ def _declare(L):
         "skr_status_string": ([c_int32], ctypes.c_char_p),
         "skr_device_info": ([POINTER(c_int32), POINTER(c_int64)], c_int32),
         "skr_spmv": ([POINTER(SkrCsr), P, P, c_int32, P], c_int32),
+        "skr_stencil_bytes": ([c_int32, c_int32, c_int32], ctypes.c_size_t),
+        "skr_stencil_build": ([POINTER(SkrCsr), c_int32, c_int32, P, ctypes.c_size_t, P], c_int32),
         "skr_residual": ([POINTER(SkrCsr), P, P, P, c_int32, P], c_int32),
         "skr_gcrodr_workspace_bytes": ([c_int32, c_int32, c_int32, c_int32], c_size_t),
         "skr_gcrodr_solve": ([POINTER(SkrCsr), P, P, P, POINTER(SkrConfig), P, c_int32, c_int32,

@@ -145,6 +145,7 @@ struct Ptrs {
   const int32_t* ci;
   const double* av;
   const double* dg;  // Jacobi diagonal or nullptr
+  StenView sv;       // optional symmetric 7-diagonal form (sv.hdr == nullptr: none)
   const double* b;
   double* x;
   double* r;
@@ -163,6 +164,11 @@ __device__ __forceinline__ double* colC(const Ptrs& p, int c) {
 }
 __device__ __forceinline__ double* colV(const Ptrs& p, int v) {
   return p.basis + (size_t)(2 * p.kcap + v) * p.ld;
+}
+
+// row of A x through the stencil form when it qualified, else the CSR
+__device__ __forceinline__ double op_row(const Ptrs& p, bool sten, const double* x, int row) {
+  return sten ? sten_row(p.sv, x, row) : csr_row(p.rp, p.ci, p.av, x, row);
 }
 
 __device__ __forceinline__ void flag_host(State* st, int cycle, int done) {
@@ -221,11 +227,12 @@ __global__ void __launch_bounds__(NT) k_init(Ptrs p, const double* x0) {
     sb += bv * bv;
     sbp += bp * bp;
   }
+  const bool sten = sten_ok(p.sv);
   for (int row = r0 + threadIdx.x; row < r1; row += NT) {
     double bv = __ldg(p.b + row);
     double rv;
     if (x0) {
-      double t = csr_row(p.rp, p.ci, p.av, x0, row);
+      double t = op_row(p, sten, x0, row);
       rv = __dsub_rn(bv, t);
     } else {
       rv = bv;
@@ -342,13 +349,17 @@ __global__ void __launch_bounds__(NT) k_spmm(Ptrs p) {
   int r = st->ncol_a;
   if (r <= 0) return;
   int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  const bool sten = sten_ok(p.sv);
   for (int row = r0 + threadIdx.x; row < r1; row += NT) {
-    int s = __ldg(p.rp + row), e = __ldg(p.rp + row + 1);
+    int s = sten ? 0 : __ldg(p.rp + row), e = sten ? 0 : __ldg(p.rp + row + 1);
     double d = p.dg ? __ldg(p.dg + row) : 1.0;
     for (int c = 0; c < r; ++c) {
       const double* Y = colU(p, c);
       double acc = 0.0;
-      for (int q = s; q < e; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(p.av + q), Y[__ldg(p.ci + q)]));
+      if (sten)
+        acc = sten_row(p.sv, Y, row);
+      else
+        for (int q = s; q < e; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(p.av + q), Y[__ldg(p.ci + q)]));
       if (p.dg) acc = __ddiv_rn(acc, d);
       colC(p, p.kcap - r + c)[row] = acc;
     }
@@ -404,8 +415,9 @@ __global__ void __launch_bounds__(NT) k_final_resid(Ptrs p) {
   __shared__ double s_red[NW];
   int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
   double s = 0.0;
+  const bool sten = sten_ok(p.sv);
   for (int row = r0 + threadIdx.x; row < r1; row += NT) {
-    double t = __dsub_rn(__ldg(p.b + row), csr_row(p.rp, p.ci, p.av, p.x, row));
+    double t = __dsub_rn(__ldg(p.b + row), op_row(p, sten, p.x, row));
     s += t * t;
   }
   double t = block_sum(s, s_red);
@@ -706,10 +718,11 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
   constexpr int SW2_COLS = R >= 4 ? 4 : 8;   // sweep-2 basis columns per load batch
   const int ntile = r1 > r0 ? (r1 - r0 + TR - 1) / TR : 0;
   // ---- cache this CTA's CSR slice in shared memory when it fits ---------------
+  const bool sten = sten_ok(p.sv);
   bool csr_local = false;
   int* lci = nullptr;
   double* lav = nullptr;
-  if (csr_cap > 0 && r1 > r0) {
+  if (!sten && csr_cap > 0 && r1 > r0) {
     const int e0 = __ldg(p.rp + r0), e1 = __ldg(p.rp + r1);
     const int rows = r1 - r0, nz = e1 - e0;
     const size_t off_ci = (size_t)(rows + 1);
@@ -733,7 +746,7 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       for (int q = a0; q < a1; ++q) acc = __dadd_rn(acc, __dmul_rn(lav[q], xv[lci[q]]));
       return acc;
     }
-    return csr_row(p.rp, p.ci, p.av, xv, row);
+    return op_row(p, sten, xv, row);
   };
   const size_t ld = p.ld;
   unsigned long long* bc = &st->bar_count;
@@ -799,7 +812,10 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
         w[i] = Vt[row[i]];
       }
       if (do_spmv) {
-        if (csr_local)
+        if (sten) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) z[i] = sten_row(p.sv, Vt, row[i]);
+        } else if (csr_local)
           spmv_rows<R, true>(csr_rp, lci, lav, Vt, row, ok, r0, z);
         else
           spmv_rows<R, false>(p.rp, p.ci, p.av, Vt, row, ok, r0, z);
@@ -1249,8 +1265,9 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
       st->prof[22] += j + 1;                // sweep iterations
       // SURVEY 8(d) algorithmic bytes: per step B_spmv + 8N(2p+6), p = basis width
       double N = (double)n;
-      double nnz = (double)(__ldg(p.rp + n));
-      double bsp = 12.0 * nnz + 4.0 * (N + 1) + 16.0 * N;
+      // (stencil form: D, W, S (, B) instead of the CSR arrays)
+      double bsp = sten ? (p.sv.sxy ? 32.0 : 24.0) * N + 16.0 * N
+                        : 12.0 * (double)(__ldg(p.rp + n)) + 4.0 * (N + 1) + 16.0 * N;
       double acc = 0.0;
       for (int q = 0; q < j; ++q) {
         int pw = kc + q + 1;
@@ -1485,23 +1502,81 @@ __global__ void __launch_bounds__(NT) k_dense_hr(const double* H, int ldh, int m
 
 // standalone SpMV / residual kernels (K1)
 __global__ void __launch_bounds__(NT) k_spmv(int n, const int32_t* rp, const int32_t* ci,
-                                              const double* av, const double* dg, const double* x,
-                                              double* y) {
+                                              const double* av, const double* dg, StenView sv,
+                                              const double* x, double* y) {
+  const bool sten = sten_ok(sv);
   for (int row = blockIdx.x * NT + threadIdx.x; row < n; row += gridDim.x * NT) {
-    double v = csr_row(rp, ci, av, x, row);
+    double v = sten ? sten_row(sv, x, row) : csr_row(rp, ci, av, x, row);
     if (dg) v = __ddiv_rn(v, __ldg(dg + row));
     y[row] = v;
   }
 }
 __global__ void __launch_bounds__(NT) k_resid(int n, const int32_t* rp, const int32_t* ci,
-                                               const double* av, const double* dg, const double* b,
-                                               const double* x, double* r) {
+                                               const double* av, const double* dg, StenView sv,
+                                               const double* b, const double* x, double* r) {
+  const bool sten = sten_ok(sv);
   for (int row = blockIdx.x * NT + threadIdx.x; row < n; row += gridDim.x * NT) {
-    double v = __dsub_rn(__ldg(b + row), csr_row(rp, ci, av, x, row));
+    double v = __dsub_rn(__ldg(b + row), sten ? sten_row(sv, x, row) : csr_row(rp, ci, av, x, row));
     if (dg) v = __ddiv_rn(v, __ldg(dg + row));
     r[row] = v;
   }
 }
+
+// stencil form (skr_stencil_build): lower entries + diagonal of every row,
+// then the upper entries checked bitwise against their mirrors
+__global__ void __launch_bounds__(NT) k_sten_lower(int n, const int32_t* rp, const int32_t* ci,
+                                                   const double* av, StenView sv) {
+  int* hdr = const_cast<int*>(sv.hdr);
+  double* D = const_cast<double*>(sv.D);
+  double* W = const_cast<double*>(sv.W);
+  double* S = const_cast<double*>(sv.S);
+  double* B = const_cast<double*>(sv.B);
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    bool bad = false, hasd = false;
+    for (int q = __ldg(rp + i), e = __ldg(rp + i + 1); q < e; ++q) {
+      const int d = __ldg(ci + q) - i;
+      const double v = __ldg(av + q);
+      if (d == 0) {
+        D[i] = v;
+        hasd = true;
+      } else if (d == 1 || d == sv.sx || (sv.sxy && d == sv.sxy)) {
+        // upper: k_sten_upper
+      } else if (v == 0.0) {
+        bad = true;  // explicit zero off the diagonal: CSR would add 0 x
+      } else if (d == -1) {
+        W[i] = v;
+      } else if (d == -sv.sx) {
+        S[i] = v;
+      } else if (sv.sxy && d == -sv.sxy) {
+        B[i] = v;
+      } else {
+        bad = true;  // off the seven diagonals
+      }
+    }
+    if (bad || !hasd) atomicOr(hdr + 1, 1);
+  }
+}
+__global__ void __launch_bounds__(NT) k_sten_upper(int n, const int32_t* rp, const int32_t* ci,
+                                                   const double* av, StenView sv) {
+  int* hdr = const_cast<int*>(sv.hdr);
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    bool bad = false;
+    int nup = 0;
+    for (int q = __ldg(rp + i), e = __ldg(rp + i + 1); q < e; ++q) {
+      const int d = __ldg(ci + q) - i;
+      if (d <= 0) continue;
+      const double v = __ldg(av + q);
+      const double m = d == 1 ? sv.W[i + 1] : d == sv.sx ? sv.S[i + sv.sx] : sv.B[i + sv.sxy];
+      if (v == 0.0 || __double_as_longlong(v) != __double_as_longlong(m)) bad = true;
+      ++nup;
+    }
+    // every lower entry of a later row must have this row's upper mirror
+    int nmir = (sv.W[i + 1] != 0.0) + (sv.S[i + sv.sx] != 0.0) +
+               (sv.sxy ? (sv.B[i + sv.sxy] != 0.0) : 0);
+    if (bad || nup != nmir) atomicOr(hdr + 1, 1);
+  }
+}
+__global__ void k_sten_final(int* hdr) { hdr[0] = hdr[1] == 0 ? 1 : 0; }
 
 // ---------------------------------------------------------------------------
 // host side
@@ -1679,9 +1754,37 @@ static int launch_combine(int kt, Ptrs p, int nblk, int cycle_mode, cudaStream_t
 
 using namespace skr;
 
+static StenView stencil_of(const skr_csr* A) {
+  if (A->stencil) return sten_view(A->stencil, A->n, A->sx, A->sxy);
+  StenView v{};
+  v.hdr = nullptr;
+  return v;
+}
+
 extern "C" {
 
-int skr_version(void) { return 100; }
+int skr_version(void) { return 101; }
+
+size_t skr_stencil_bytes(int32_t n, int32_t sx, int32_t sxy) {
+  if (n < 1 || sx < 2 || (sxy != 0 && sxy <= sx)) return 0;
+  return sten_doubles(n, sx, sxy) * sizeof(double);
+}
+
+int skr_stencil_build(const skr_csr* A, int32_t sx, int32_t sxy, void* buf, size_t bytes,
+                      void* stream) {
+  if (!A || !buf || A->n < 1 || !A->row_ptr || !A->col_idx || !A->values) return SKR_ERR_ARG;
+  size_t need = skr_stencil_bytes(A->n, sx, sxy);
+  if (need == 0) return SKR_ERR_ARG;
+  if (bytes < need) return SKR_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(buf, 0, need, s) != cudaSuccess) return SKR_ERR_CUDA;
+  StenView v = sten_view(buf, A->n, sx, sxy);
+  int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
+  k_sten_lower<<<grid, NT, 0, s>>>(A->n, A->row_ptr, A->col_idx, A->values, v);
+  k_sten_upper<<<grid, NT, 0, s>>>(A->n, A->row_ptr, A->col_idx, A->values, v);
+  k_sten_final<<<1, 1, 0, s>>>(const_cast<int*>(v.hdr));
+  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+}
 
 const char* skr_status_string(int s) {
   switch (s) {
@@ -1709,7 +1812,8 @@ int skr_spmv(const skr_csr* A, const double* x, double* y, int apply_prec, void*
   if (A->n == 0) return SKR_OK;
   int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
   k_spmv<<<grid, NT, 0, (cudaStream_t)stream>>>(A->n, A->row_ptr, A->col_idx, A->values,
-                                                 apply_prec ? A->diag : nullptr, x, y);
+                                                 apply_prec ? A->diag : nullptr, stencil_of(A), x,
+                                                 y);
   return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
 }
 
@@ -1719,7 +1823,8 @@ int skr_residual(const skr_csr* A, const double* b, const double* x, double* r, 
   if (A->n == 0) return SKR_OK;
   int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
   k_resid<<<grid, NT, 0, (cudaStream_t)stream>>>(A->n, A->row_ptr, A->col_idx, A->values,
-                                                  apply_prec ? A->diag : nullptr, b, x, r);
+                                                  apply_prec ? A->diag : nullptr, stencil_of(A), b,
+                                                  x, r);
   return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
 }
 
@@ -1770,6 +1875,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.ci = A->col_idx;
   p.av = A->values;
   p.dg = A->diag;
+  p.sv = stencil_of(A);
   p.b = b;
   p.x = x;
   p.r = (double*)(base + L.r);

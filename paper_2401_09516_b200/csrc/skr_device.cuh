@@ -36,6 +36,74 @@ __device__ __forceinline__ double csr_row(const int32_t* __restrict__ rp,
   return acc;
 }
 
+// Symmetric 7-diagonal ("stencil") form of a CSR matrix whose entries lie on
+// the diagonals {0, +-1, +-sx, +-sxy} (5-/7-point finite-difference operators
+// in natural ordering), with A(i, i+d) == A(i+d, i) bitwise, nonzero
+// off-diagonal entries and a diagonal entry in every row. Stored as the
+// diagonal D and the lower entries W (d = -1), S (-sx), B (-sxy), each
+// zero-padded past n so the upper entries W[i+1], S[i+sx], B[i+sxy] need no
+// bounds test; a zero coefficient marks an absent entry. Built and verified
+// on the device by skr_stencil_build; hdr[0] == 1 when the matrix qualified.
+// 24 (2-D) or 32 (3-D) bytes per row instead of CSR's 64 / 88.
+struct StenView {
+  const int* hdr;  // nullptr: no stencil form
+  const double* D;
+  const double* W;
+  const double* S;
+  const double* B;  // nullptr in 2-D (sxy == 0)
+  int n, sx, sxy;
+};
+constexpr int STEN_HDR_DOUBLES = 8;  // 64-byte header: int ok, int fail, ...
+
+__host__ __device__ inline size_t sten_doubles(int n, int sx, int sxy) {
+  return (size_t)STEN_HDR_DOUBLES + (size_t)n + (size_t)(n + 1) + (size_t)(n + sx) +
+         (sxy ? (size_t)(n + sxy) : 0);
+}
+__host__ __device__ inline StenView sten_view(const void* buf, int n, int sx, int sxy) {
+  StenView v;
+  const double* d = (const double*)buf;
+  v.hdr = (const int*)buf;
+  v.D = d + STEN_HDR_DOUBLES;
+  v.W = v.D + n;
+  v.S = v.W + (n + 1);
+  v.B = sxy ? v.S + (n + sx) : nullptr;
+  v.n = n;
+  v.sx = sx;
+  v.sxy = sxy;
+  return v;
+}
+__device__ __forceinline__ bool sten_ok(const StenView& v) {
+  return v.hdr != nullptr && *(const volatile int*)v.hdr == 1;
+}
+
+// Row i of A x in CSR column order (i - sxy, i - sx, i - 1, i, i + 1, i + sx,
+// i + sxy) with the same separate round-to-nearest multiply and add as
+// csr_row and absent entries skipped: bit-identical to csr_row on the CSR the
+// form was built from. x loads are clamped in range and issued up front.
+__device__ __forceinline__ double sten_row(const StenView& v, const double* x, int i) {
+  const int n1 = v.n - 1;
+  double cb = 0.0, ct = 0.0, xb = 0.0, xt = 0.0;
+  if (v.sxy) {
+    cb = __ldg(v.B + i);
+    ct = __ldg(v.B + i + v.sxy);
+    xb = x[max(i - v.sxy, 0)];
+    xt = x[min(i + v.sxy, n1)];
+  }
+  const double cs = __ldg(v.S + i), cn = __ldg(v.S + i + v.sx);
+  const double cw = __ldg(v.W + i), ce = __ldg(v.W + i + 1), cd = __ldg(v.D + i);
+  const double xs = x[max(i - v.sx, 0)], xn = x[min(i + v.sx, n1)];
+  const double xw = x[max(i - 1, 0)], xe = x[min(i + 1, n1)], xd = x[i];
+  double acc = 0.0;
+  if (cb != 0.0) acc = __dadd_rn(acc, __dmul_rn(cb, xb));
+  if (cs != 0.0) acc = __dadd_rn(acc, __dmul_rn(cs, xs));
+  if (cw != 0.0) acc = __dadd_rn(acc, __dmul_rn(cw, xw));
+  acc = __dadd_rn(acc, __dmul_rn(cd, xd));
+  if (ce != 0.0) acc = __dadd_rn(acc, __dmul_rn(ce, xe));
+  if (cn != 0.0) acc = __dadd_rn(acc, __dmul_rn(cn, xn));
+  if (ct != 0.0) acc = __dadd_rn(acc, __dmul_rn(ct, xt));
+  return acc;
+}
+
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

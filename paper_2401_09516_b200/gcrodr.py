@@ -223,7 +223,7 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
             dA = dA.with_diag(M.device_diag() if isinstance(M, JacobiPreconditioner)
                               else None)
         if not jacobi and dA.diag is not None:
-            dA = DeviceCsr(dA.n, dA.row_ptr, dA.col_idx, dA.values, None)
+            dA = dA.with_diag(None)
     else:
         host = CsrMatrix.of(A)
         if host.n_rows != host.n_cols:

@@ -11,6 +11,7 @@ Jacobi diagonal, uploaded once per system.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Sequence
 
 import numpy as np
@@ -113,19 +114,69 @@ class CsrMatrix:
         return f"CsrMatrix(shape={self.shape}, nnz={self.nnz})"
 
 
-class DeviceCsr:
-    """Device-resident CSR (int32 indices, fp64 values) + optional Jacobi diagonal."""
+def stencil_offsets(row_ptr, col_idx):
+    """Diagonal offsets (sx, sxy) of a 5-/7-point stencil matrix in natural
+    ordering, read off row 0's upper entries (columns 1, sx[, sxy]), or None.
+    Only a guess: skr_stencil_build verifies every row on the device."""
+    if len(row_ptr) < 2:
+        return None
+    e = int(row_ptr[1])
+    cols = np.asarray(col_idx[:e]).astype(np.int64)
+    up = cols[cols > 0]
+    if len(up) == 2 and up[0] == 1 and up[1] >= 2:
+        return int(up[1]), 0
+    if len(up) == 3 and up[0] == 1 and up[1] >= 2 and up[2] > up[1]:
+        return int(up[1]), int(up[2])
+    return None
 
-    def __init__(self, n, row_ptr, col_idx, values, diag=None, keep=None):
+
+def stencil_enabled() -> bool:
+    """The stencil form is used unless SKR_NO_STENCIL=1 (A/B runs, tests)."""
+    return os.environ.get("SKR_NO_STENCIL", "0") in ("", "0")
+
+
+class DeviceCsr:
+    """Device-resident CSR (int32 indices, fp64 values) + optional Jacobi
+    diagonal + optional stencil form (skr_stencil_build; the kernels use it
+    only if the device check found the matrix to be a symmetric 7-diagonal
+    one, with bit-identical results)."""
+
+    def __init__(self, n, row_ptr, col_idx, values, diag=None, keep=None, stencil=None):
         self.n = int(n)
         self.row_ptr = row_ptr
         self.col_idx = col_idx
         self.values = values
         self.diag = diag
         self._keep = keep
+        self.stencil = stencil  # (device buffer, sx, sxy) or None
+        buf, sx, sxy = stencil if stencil is not None else (None, 0, 0)
         self.c = _lib.SkrCsr(self.n, int(values.numel()), row_ptr.data_ptr(),
                              col_idx.data_ptr(), values.data_ptr(),
-                             diag.data_ptr() if diag is not None else None)
+                             diag.data_ptr() if diag is not None else None,
+                             buf.data_ptr() if buf is not None else None, int(sx), int(sxy))
+
+    def stencil_active(self) -> bool:
+        """True when the device check accepted the stencil form (syncs)."""
+        if self.stencil is None:
+            return False
+        return int(self.stencil[0][:4].view(__import__("torch").int32).item()) == 1
+
+    def build_stencil(self, offsets, stream=None):
+        """Build (and verify on the device) the stencil form for `offsets`."""
+        import torch
+
+        sx, sxy = offsets
+        L = _lib.load()
+        nbytes = int(L.skr_stencil_bytes(self.n, sx, sxy))
+        if nbytes == 0:
+            return self
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=self.values.device)
+        probe = _lib.SkrCsr(self.n, int(self.values.numel()), self.row_ptr.data_ptr(),
+                            self.col_idx.data_ptr(), self.values.data_ptr(), None, None, 0, 0)
+        _lib.check(L.skr_stencil_build(ctypes.byref(probe), sx, sxy, buf.data_ptr(), nbytes,
+                                       _lib.stream_handle(stream)), "skr_stencil_build")
+        return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, self.diag, self._keep,
+                         (buf, sx, sxy))
 
     @property
     def nnz(self) -> int:
@@ -164,10 +215,15 @@ class DeviceCsr:
 
                     zero = int(torch.nonzero(diag == 0)[0].item())
                     raise ZeroPivotError("jacobi", zero)
-        return cls(n, rp, ci, vals, diag)
+            dA = cls(n, rp, ci, vals, diag)
+            off = stencil_offsets(A.row_ptr, A.col_idx) if stencil_enabled() else None
+            if off is not None:
+                dA = dA.build_stencil(off, stream=stream)
+        return dA
 
     def with_diag(self, diag):
-        return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, diag)
+        return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, diag, self._keep,
+                         self.stencil)
 
 
 class _nullctx:

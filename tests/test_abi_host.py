@@ -25,7 +25,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/skr.h but not exported"
     assert set(_lib.EXPORTS) == set(syms)
-    assert L.skr_version() == 100
+    assert L.skr_version() == 101
     assert L.skr_status_string(0) == b"ok"
 
 

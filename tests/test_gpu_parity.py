@@ -77,6 +77,92 @@ def test_spmv_edge_cases():
         skr.spmv(A, np.ones(3))
 
 
+# ------------------------------------------------------- stencil form of the operator
+def _spmv_dev(dA, x, prec=0):
+    import ctypes
+
+    skr = _skr()
+    L = skr._lib.load()
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    yt = torch.empty_like(xt)
+    skr._lib.check(L.skr_spmv(ctypes.byref(dA.c), xt.data_ptr(), yt.data_ptr(), prec,
+                              skr._lib.stream_handle()), "spmv")
+    return yt.cpu().numpy()
+
+
+@pytest.mark.parametrize("cid,n", [(0, None), (1, 48), (2, 40), (3, 12), (4, 96)])
+def test_stencil_spmv_bitexact(cid, n):
+    """The 7-diagonal form reproduces the CSR row sums (and scipy) bit for bit."""
+    skr = _skr()
+    spec = _spec(cid, n=n) if n else _spec(cid)
+    A, _, _ = _system(spec, 3)
+    dA = skr.DeviceCsr.from_host(A, jacobi=True)
+    assert dA.stencil is not None and dA.stencil_active(), "FD matrix must take the stencil path"
+    plain = skr.DeviceCsr(dA.n, dA.row_ptr, dA.col_idx, dA.values, dA.diag)
+    rng = np.random.default_rng(cid)
+    for x in (rng.standard_normal(A.n_rows), np.ones(A.n_rows), np.zeros(A.n_rows)):
+        ref = A.to_scipy() @ x
+        assert np.array_equal(_spmv_dev(dA, x), ref)
+        assert np.array_equal(_spmv_dev(plain, x), ref)
+        assert np.array_equal(_spmv_dev(dA, x, 1), _spmv_dev(plain, x, 1))
+
+
+def test_stencil_rejects_non_stencil_matrices():
+    """Asymmetric values, an explicit zero, an off-pattern entry or a missing
+    diagonal leave the stencil form disabled; results stay exact (CSR path)."""
+    skr = _skr()
+    spec = _spec(0, n=16)
+    A, _, _ = _system(spec, 1)
+    rp, ci, v = A.row_ptr.copy(), A.col_idx.copy(), A.values.copy()
+    x = np.random.default_rng(7).standard_normal(A.n_rows)
+
+    def check(rp_, ci_, v_, active):
+        M = skr.CsrMatrix(A.n_rows, A.n_cols, rp_, ci_, v_)
+        dM = skr.DeviceCsr.from_host(M)
+        assert dM.stencil_active() == active
+        assert np.array_equal(_spmv_dev(dM, x), M.to_scipy() @ x)
+
+    check(rp, ci, v, True)
+    r = 20  # an interior row: perturb its east entry only (breaks symmetry)
+    q = [e for e in range(rp[r], rp[r + 1]) if ci[e] == r + 1][0]
+    v2 = v.copy()
+    v2[q] = np.nextafter(v2[q], 0.0)
+    check(rp, ci, v2, False)
+    v3 = v.copy()
+    v3[q] = 0.0  # explicit zero entry
+    w = [e for e in range(rp[r + 1], rp[r + 2]) if ci[e] == r][0]
+    v3[w] = 0.0
+    check(rp, ci, v3, False)
+    # a diagonal dropped from one row
+    d = [e for e in range(rp[r], rp[r + 1]) if ci[e] == r][0]
+    keep = np.ones(len(v), bool)
+    keep[d] = False
+    rp4 = rp.copy()
+    rp4[r + 1:] -= 1
+    check(rp4, ci[keep], v[keep], False)
+
+
+def test_stencil_solve_matches_csr_solve():
+    """A chain solved through the stencil form converges like the CSR one."""
+    skr = _skr()
+    spec = _spec(1, n=48)
+    cfg = skr.SolverConfig(m=spec.m, k=spec.k, tol=spec.tol, max_iter=spec.max_iter)
+    out = {}
+    for mode in ("1", "0"):
+        os.environ["SKR_NO_STENCIL"] = mode
+        try:
+            systems = [_system(spec, i)[:2] for i in range(3)]
+            res = skr.solve_sequence(systems, [0, 1, 2], cfg, spec.precond, keep_x="host")
+        finally:
+            os.environ.pop("SKR_NO_STENCIL", None)
+        out[mode] = res
+    a, b = out["1"], out["0"]  # CSR, stencil
+    assert all(a.converged) and all(b.converged)
+    for ia, ib, xa, xb in zip(a.iterations, b.iterations, a.x, b.x):
+        assert abs(ia - ib) <= max(2, 0.05 * ia)
+        assert np.linalg.norm(xa - xb) <= 1e-6 * np.linalg.norm(xa)
+
+
 # ----------------------------------------------------------------------------- sort
 def test_sort_c0_golden():
     skr = _skr()

@@ -59,6 +59,38 @@ def greedy_order(flat: np.ndarray) -> list[int]:
     return chain
 
 
+def grouped_order(flat: np.ndarray, group_size: int) -> list[int]:
+    """Greedy sort within coarse groups (sorting.py:83-111).
+
+    Rows are bucketed by their coordinate along the first principal direction
+    (right singular vector of the centered batch, sign fixed so its largest-
+    magnitude component is positive, sorting.py:99-104), stable-argsorted,
+    cut into contiguous groups of ``group_size``; each group (ascending
+    original indices) is greedy-chained from its smallest index
+    (sorting.py:55-69) and the chains are concatenated (sorting.py:106-110).
+    """
+    if group_size < 2:
+        raise ValueError("group_size must be >= 2")
+    flat = np.asarray(flat, dtype=np.float64)
+    n = flat.shape[0]
+    if n <= group_size:
+        return greedy_order(flat)
+    centered = flat - flat.mean(axis=0)
+    _, _, vt = np.linalg.svd(centered, full_matrices=False)
+    direction = vt[0]
+    lead = np.argmax(np.abs(direction))
+    if direction[lead] < 0:
+        direction = -direction
+    key = centered @ direction
+    by_key = np.argsort(key, kind="stable")
+    order: list[int] = []
+    for start in range(0, n, group_size):
+        group = np.sort(by_key[start:start + group_size])
+        sub = greedy_order(flat[group])
+        order.extend(int(group[i]) for i in sub)
+    return order
+
+
 def greedy_order_prefix(flat: np.ndarray, npos: int) -> list[int]:
     """The first ``npos`` positions of greedy_order (the chain is sequential, so
     a prefix costs npos passes instead of n); same arithmetic."""

@@ -38,6 +38,8 @@ from .sorting import (
     frobenius_distance,
     greedy_sort,
     greedy_sort_device,
+    grouped_sort,
+    grouped_sort_device,
     sharded_greedy_sort,
 )
 from .sparse import CsrMatrix, DeviceCsr, axpy, dot, eye, norm2, spmv
@@ -49,6 +51,6 @@ __all__ = [
     "ParameterMatrix", "Preconditioner", "RecycleSpace", "SequenceResult", "SolveReport",
     "SolverConfig", "ZeroPivotError", "axpy", "build_preconditioner", "chunk_positions", "dot",
     "eye", "frobenius_distance", "gcrodr_solve", "gmres_solve", "greedy_sort",
-    "greedy_sort_device", "harmonic_ritz_first_cycle", "harmonic_ritz_subsequent", "norm2",
+    "greedy_sort_device", "grouped_sort", "grouped_sort_device", "harmonic_ritz_first_cycle", "harmonic_ritz_subsequent", "norm2",
     "sharded_greedy_sort", "chain_grid_ctas", "solve_chains", "solve_sequence", "split_chunks", "spmv",
 ]

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 
 __all__ = ["ParameterMatrix", "frobenius_distance", "gather_distance_rows", "greedy_sort",
-           "greedy_sort_device",
+           "greedy_sort_device", "grouped_sort", "grouped_sort_device",
            "sharded_greedy_sort", "row_shard"]
 
 
@@ -100,6 +100,57 @@ def greedy_sort(params: Sequence[ParameterMatrix]) -> list[int]:
     flat = _stacked(params)
     _lib.require_cuda()
     return greedy_sort_device(torch.from_numpy(flat).to("cuda"))
+
+
+def grouped_sort_device(flat_dev, group_size: int, stream=None) -> list[int]:
+    """``grouped_sort`` of the rows of a (n_sys, P) float64 CUDA tensor.
+
+    The principal direction (sorting.py:99-101) is the top eigenvector of the
+    smaller Gram matrix of the centered batch (cuBLAS DGEMM + cuSOLVER eigh
+    through torch: O(n_sys^2 P) once); the sign rule, the stable key order and
+    the contiguous groups follow sorting.py:102-110, and every group's chain
+    runs in the device greedy-sort kernels (rows gathered in ascending original
+    index, so the lowest-index tie-break is the reference's)."""
+    import torch
+
+    if group_size < 2:
+        raise ValueError("group_size must be >= 2")
+    n, P = flat_dev.shape
+    if n <= group_size:
+        return greedy_sort_device(flat_dev, stream)
+    C = flat_dev - flat_dev.mean(dim=0, keepdim=True)
+    if P <= n:
+        _, V = torch.linalg.eigh(C.T @ C)
+        d = V[:, -1]
+    else:
+        _, U = torch.linalg.eigh(C @ C.T)
+        d = C.T @ U[:, -1]
+        nrm = torch.linalg.norm(d)
+        d = d / nrm if float(nrm) > 0 else d
+    lead = int(torch.argmax(d.abs()))
+    if float(d[lead]) < 0:
+        d = -d
+    key = C @ d
+    by_key = torch.argsort(key, stable=True)
+    order: list[int] = []
+    for start in range(0, n, group_size):
+        g = torch.sort(by_key[start:start + group_size]).values
+        sub = greedy_sort_device(flat_dev.index_select(0, g), stream)
+        gl = g.cpu().tolist()
+        order.extend(int(gl[i]) for i in sub)
+    return order
+
+
+def grouped_sort(params: Sequence[ParameterMatrix], group_size: int) -> list[int]:
+    """Greedy sort within coarse groups; O(N * group_size) distance
+    evaluations (sorting.py:83-111), on the GPU."""
+    import torch
+
+    if group_size < 2:
+        raise ValueError("group_size must be >= 2")
+    flat = _stacked(params)
+    _lib.require_cuda()
+    return grouped_sort_device(torch.from_numpy(flat).to("cuda"), group_size)
 
 
 def row_shard(n: int, world: int, rank: int) -> tuple[int, int]:

@@ -188,6 +188,25 @@ def test_sort_golden(tag, cid, n, ns):
     assert order == list(g[f"{tag}_order"])
 
 
+def test_grouped_sort_golden():
+    """Device grouped_sort reproduces the reference's permutations (sorting.py:83-111)."""
+    skr = _skr()
+    from paper_2401_09516_b200 import problems as P
+
+    g = np.load(os.path.join(GOLD, "grouped.npz"))
+    for tag, spec, ns, sizes in (("c1r", P.CONFIGS[1].reduced(n=32), 200, (16, 50, 200)),
+                                 ("c2r", P.CONFIGS[2].reduced(n=16), 96, (8, 40)),
+                                 ("c4r", P.CONFIGS[4].reduced(n=24), 300, (2, 64))):
+        flat = np.stack([P.system_params(spec, i)["params"] for i in range(ns)])
+        params = [skr.ParameterMatrix(f) for f in flat]
+        for gs in sizes:
+            assert skr.grouped_sort(params, gs) == g[f"{tag}_g{gs}"].tolist(), (tag, gs)
+    dup = [skr.ParameterMatrix(f) for f in g["dup_flat"]]
+    assert skr.grouped_sort(dup, 7) == g["dup_g7"].tolist()
+    with pytest.raises(ValueError):
+        skr.grouped_sort(dup, 1)
+
+
 def test_sort_ties_and_scalars():
     skr = _skr()
     g = np.load(os.path.join(GOLD, "sort.npz"))

@@ -124,3 +124,20 @@ def test_dense_golden_against_oracle_functions():
         np.testing.assert_allclose(np.abs(P1), np.abs(d[f"hf{t}_P"]), atol=1e-10)
         P2 = orc.hr_next(d[f"hs{t}_G"], d[f"hs{t}_cross"], int(d[f"hs{t}_k"]))
         np.testing.assert_allclose(np.abs(P2), np.abs(d[f"hs{t}_P"]), atol=1e-10)
+
+
+def test_oracle_grouped_sort_golden():
+    """oracle.grouped_order reproduces the reference's grouped_sort (sorting.py:83-111)."""
+    from paper_2401_09516_b200 import problems as P
+
+    g = load("grouped.npz")
+    for tag, spec, ns, sizes in (("c1r", P.CONFIGS[1].reduced(n=32), 200, (16, 50, 200)),
+                                 ("c2r", P.CONFIGS[2].reduced(n=16), 96, (8, 40)),
+                                 ("c4r", P.CONFIGS[4].reduced(n=24), 300, (2, 64))):
+        flat = np.stack([P.system_params(spec, i)["params"] for i in range(ns)])
+        assert sha(flat) == str(g[f"{tag}_sha"]), "generator drift"
+        for gs in sizes:
+            assert orc.grouped_order(flat, gs) == g[f"{tag}_g{gs}"].tolist(), (tag, gs)
+    assert orc.grouped_order(g["dup_flat"], 7) == g["dup_g7"].tolist()
+    with pytest.raises(ValueError):
+        orc.grouped_order(g["dup_flat"], 1)

@@ -127,6 +127,19 @@ size_t skr_stencil_bytes(int32_t n, int32_t sx, int32_t sxy);
 int skr_stencil_build(const skr_csr* A, int32_t sx, int32_t sxy, void* buf, size_t bytes,
                       void* stream);
 
+/* Device assembly of the benchmark configs' FD systems (problems.py assemble;
+ * reference problems.py:335-355, :380-383): from the per-cell coefficient
+ * field (kind 0: a of -div(a grad u), harmonic-mean faces, wall faces = cell
+ * value, negative h^2-scaled diagonal; kind 1: Helmholtz wavenumber k(x),
+ * off-diagonals 1, diagonal -2 dim + (k h)^2) on an n^dim interior grid in
+ * natural ordering, writes the stencil form (verified flag set; stencil_bytes
+ * >= skr_stencil_bytes(n^dim, n, dim == 3 ? n^2 : 0)) and, when values is not
+ * NULL, the CSR values in the fixed pattern row_ptr. Bit-identical to the host
+ * assembly (same operation order, no FMA contraction). */
+int skr_assemble_fd(int32_t kind, int32_t dim, int32_t n, const double* field, double h,
+                    const int32_t* row_ptr, double* values, void* stencil, size_t stencil_bytes,
+                    void* stream);
+
 size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter);
 /* Solve A x = b with GCRO-DR. U_in (n x k_in, column-major, leading dim ldu)
  * is the previous system's recycle U (its C is not needed: the refresh

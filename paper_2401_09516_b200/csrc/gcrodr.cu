@@ -739,7 +739,26 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
     }
     __syncthreads();
   }
+  // ---- or its slice of the 2-D stencil form: D, W (+1), S (+sx) ------------
+  bool sten_local = false;
+  const double *lD = nullptr, *lW = nullptr, *lS = nullptr;
+  if (sten && !p.sv.sxy && csr_cap > 0 && r1 > r0) {
+    const int rows = r1 - r0, sx = p.sv.sx;
+    if ((size_t)(3 * rows + 1 + sx) * sizeof(double) <= (size_t)csr_cap) {
+      double* c0 = reinterpret_cast<double*>(csr_rp);
+      for (int q = tid; q < rows; q += NT) c0[q] = __ldg(p.sv.D + r0 + q);
+      for (int q = tid; q <= rows; q += NT) c0[rows + q] = __ldg(p.sv.W + r0 + q);
+      for (int q = tid; q < rows + sx; q += NT) c0[2 * rows + 1 + q] = __ldg(p.sv.S + r0 + q);
+      lD = c0;
+      lW = c0 + rows;
+      lS = c0 + 2 * rows + 1;
+      sten_local = true;
+    }
+    __syncthreads();
+  }
   auto row_dot = [&](const double* xv, int row) -> double {
+    if (sten_local)
+      return sten_row_at<false>(lD, lW, lS, nullptr, p.sv.sx, 0, n, xv, row, row - r0);
     if (csr_local) {
       int a0 = csr_rp[row - r0], a1 = csr_rp[row - r0 + 1];
       double acc = 0.0;
@@ -812,7 +831,11 @@ __global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_c
         w[i] = Vt[row[i]];
       }
       if (do_spmv) {
-        if (sten) {
+        if (sten_local) {
+#pragma unroll
+          for (int i = 0; i < R; ++i)
+            z[i] = sten_row_at<false>(lD, lW, lS, nullptr, p.sv.sx, 0, n, Vt, row[i], row[i] - r0);
+        } else if (sten) {
 #pragma unroll
           for (int i = 0; i < R; ++i) z[i] = sten_row(p.sv, Vt, row[i]);
         } else if (csr_local)

@@ -80,18 +80,24 @@ __device__ __forceinline__ bool sten_ok(const StenView& v) {
 // i + sxy) with the same separate round-to-nearest multiply and add as
 // csr_row and absent entries skipped: bit-identical to csr_row on the CSR the
 // form was built from. x loads are clamped in range and issued up front.
-__device__ __forceinline__ double sten_row(const StenView& v, const double* x, int i) {
-  const int n1 = v.n - 1;
+// Coefficients are read at index c (c = i for the global arrays, i - r0 for a
+// CTA's shared-memory slice whose S part starts at row r0 as well).
+template <bool GLOBAL>
+__device__ __forceinline__ double sten_row_at(const double* D, const double* W, const double* S,
+                                              const double* B, int sx, int sxy, int n,
+                                              const double* x, int i, int c) {
+  const int n1 = n - 1;
+  auto ld = [](const double* q) { return GLOBAL ? __ldg(q) : *q; };
   double cb = 0.0, ct = 0.0, xb = 0.0, xt = 0.0;
-  if (v.sxy) {
-    cb = __ldg(v.B + i);
-    ct = __ldg(v.B + i + v.sxy);
-    xb = x[max(i - v.sxy, 0)];
-    xt = x[min(i + v.sxy, n1)];
+  if (sxy) {
+    cb = ld(B + c);
+    ct = ld(B + c + sxy);
+    xb = x[max(i - sxy, 0)];
+    xt = x[min(i + sxy, n1)];
   }
-  const double cs = __ldg(v.S + i), cn = __ldg(v.S + i + v.sx);
-  const double cw = __ldg(v.W + i), ce = __ldg(v.W + i + 1), cd = __ldg(v.D + i);
-  const double xs = x[max(i - v.sx, 0)], xn = x[min(i + v.sx, n1)];
+  const double cs = ld(S + c), cn = ld(S + c + sx);
+  const double cw = ld(W + c), ce = ld(W + c + 1), cd = ld(D + c);
+  const double xs = x[max(i - sx, 0)], xn = x[min(i + sx, n1)];
   const double xw = x[max(i - 1, 0)], xe = x[min(i + 1, n1)], xd = x[i];
   double acc = 0.0;
   if (cb != 0.0) acc = __dadd_rn(acc, __dmul_rn(cb, xb));
@@ -102,6 +108,9 @@ __device__ __forceinline__ double sten_row(const StenView& v, const double* x, i
   if (cn != 0.0) acc = __dadd_rn(acc, __dmul_rn(cn, xn));
   if (ct != 0.0) acc = __dadd_rn(acc, __dmul_rn(ct, xt));
   return acc;
+}
+__device__ __forceinline__ double sten_row(const StenView& v, const double* x, int i) {
+  return sten_row_at<true>(v.D, v.W, v.S, v.B, v.sx, v.sxy, v.n, x, i, i);
 }
 
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {

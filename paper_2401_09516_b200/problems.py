@@ -39,6 +39,8 @@ __all__ = [
     "grf",
     "system_params",
     "assemble",
+    "assemble_device",
+    "rhs",
     "csr_pattern",
 ]
 
@@ -200,6 +202,84 @@ def _faces_flux(a: np.ndarray):
         hi[tuple(last)] = a[tuple(last)]
         faces.append((lo, hi))
     return faces
+
+
+def rhs(spec: ConfigSpec, fields: dict) -> np.ndarray:
+    """Right-hand side b of a system (the b of ``assemble``)."""
+    dim, n = spec.dim, spec.n
+    N = n ** dim
+    h = 1.0 / (n + 1)
+    if spec.kind == "darcy_binary":
+        return -(h * h) * np.ones(N)
+    if spec.kind == "poisson_lognormal":
+        return -(h * h) * np.random.default_rng([BASE_SEED, spec.cid, 7, 0]).standard_normal(N)
+    if spec.kind == "helmholtz":
+        coords = [(np.arange(1, n + 1) * h)] * dim
+        grids = np.meshgrid(*coords, indexing="ij")
+        c = fields["center"]
+        r2 = np.zeros((n,) * dim)
+        for arr_ax in range(dim):
+            ax = dim - 1 - arr_ax
+            r2 = r2 + (grids[arr_ax] - c[ax]) ** 2
+        return (h * h) * np.exp(-r2 / (2.0 * spec.bump_sigma ** 2)).ravel()
+    raise ValueError(spec.kind)
+
+
+_PATTERN_DEV: dict = {}
+
+
+def assemble_device(spec: ConfigSpec, idx: int, fields: dict | None = None, stream=None,
+                    jacobi: bool | None = None):
+    """Assemble system ``idx`` on the GPU (``skr_assemble_fd``): only the
+    coefficient field (and b) is uploaded; the CSR values and the stencil form
+    are written by the device, bit-identical to ``assemble``. Returns
+    (DeviceCsr, b on the device, params)."""
+    import torch
+
+    from . import _lib
+    from .sparse import DeviceCsr
+
+    _lib.require_cuda()
+    L = _lib.load()
+    fields = fields if fields is not None else system_params(spec, idx)
+    dim, n = spec.dim, spec.n
+    N = n ** dim
+    h = 1.0 / (n + 1)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = (dim, n, dev.index)
+    if key not in _PATTERN_DEV:
+        rp, ci, _ = csr_pattern(dim, n)
+        _PATTERN_DEV[key] = (torch.from_numpy(rp.astype(np.int32)).to(dev),
+                             torch.from_numpy(ci.astype(np.int32)).to(dev))
+    rp_d, ci_d = _PATTERN_DEV[key]
+    kind = 1 if spec.kind == "helmholtz" else 0
+    field = fields["kfield"] if kind else fields["a"]
+    ctx = torch.cuda.stream(stream) if stream is not None else _null()
+    with ctx:
+        f_d = torch.from_numpy(np.ascontiguousarray(field, dtype=np.float64).ravel()).to(
+            dev, non_blocking=True)
+        vals = torch.empty(ci_d.numel(), dtype=torch.float64, device=dev)
+        sx, sxy = n, (n * n if dim == 3 else 0)
+        nbytes = int(L.skr_stencil_bytes(N, sx, sxy))
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _lib.check(L.skr_assemble_fd(kind, dim, n, f_d.data_ptr(), h, rp_d.data_ptr(),
+                                     vals.data_ptr(), buf.data_ptr(), nbytes,
+                                     _lib.stream_handle(stream)), "skr_assemble_fd")
+        b_d = torch.from_numpy(rhs(spec, fields)).to(dev, non_blocking=True)
+        jac = (spec.precond == "jacobi") if jacobi is None else jacobi
+        # Jacobi diagonal = the stencil form's D (strictly negative for the flux
+        # operators: minus a sum of positive face coefficients)
+        diag = buf[64:64 + 8 * N].view(torch.float64) if jac else None
+        dA = DeviceCsr(N, rp_d, ci_d, vals, diag, keep=(f_d,), stencil=(buf, sx, sxy))
+    return dA, b_d, fields["params"]
+
+
+class _null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 
 
 def assemble(spec: ConfigSpec, idx: int, fields: dict | None = None):

@@ -142,6 +142,33 @@ def test_stencil_rejects_non_stencil_matrices():
     check(rp4, ci[keep], v[keep], False)
 
 
+@pytest.mark.parametrize("cid,n", [(0, None), (1, 40), (2, 24), (3, 10), (4, 64)])
+def test_device_assembly_bitexact(cid, n):
+    """skr_assemble_fd reproduces the host assembly bit for bit (CSR values,
+    stencil form, b) from the uploaded coefficient field."""
+    skr = _skr()
+    from paper_2401_09516_b200 import problems as P
+
+    spec = _spec(cid, n=n) if n else _spec(cid)
+    for idx in (0, 5):
+        rp, ci, v, b, prm = P.assemble(spec, idx)
+        dA, bd, prm_d = P.assemble_device(spec, idx)
+        assert np.array_equal(dA.values.cpu().numpy(), v)
+        assert np.array_equal(dA.row_ptr.cpu().numpy(), rp)
+        assert np.array_equal(dA.col_idx.cpu().numpy(), ci)
+        assert np.array_equal(bd.cpu().numpy(), b)
+        assert np.array_equal(prm_d, prm)
+        assert dA.stencil_active()
+        if spec.precond == "jacobi":
+            A = skr.CsrMatrix(spec.N, spec.N, rp, ci, v)
+            assert np.array_equal(dA.diag.cpu().numpy(), A.diagonal())
+        # the device-built stencil form equals the one verified from the CSR
+        chk = skr.DeviceCsr(dA.n, dA.row_ptr, dA.col_idx, dA.values).build_stencil(
+            (dA.stencil[1], dA.stencil[2]))
+        assert chk.stencil_active()
+        assert torch.equal(chk.stencil[0][64:], dA.stencil[0][64:])
+
+
 def test_stencil_solve_matches_csr_solve():
     """A chain solved through the stencil form converges like the CSR one."""
     skr = _skr()

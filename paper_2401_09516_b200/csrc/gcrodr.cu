@@ -680,12 +680,18 @@ inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
   return L;
 }
 // dynamic smem per CTA that keeps 2 CTAs (+ ~7.6 KB static each) on an SM
-constexpr size_t CYCLE_DSMEM_BUDGET = 96 * 1024;
+#ifndef SKR_CYCLE_DSMEM_KB
+#define SKR_CYCLE_DSMEM_KB 96
+#endif
+constexpr size_t CYCLE_DSMEM_BUDGET = SKR_CYCLE_DSMEM_KB * 1024;
 
 // R = rows per lane in the Arnoldi sweeps: warp-owned tiles of 32 R consecutive
 // rows; every lane keeps its rows' w = V_t and z = op(V_t) in registers.
 template <int R>
-__global__ void __launch_bounds__(NT, 2) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
+#ifndef SKR_CYCLE_MINB
+#define SKR_CYCLE_MINB 2  // CTAs per SM the register allocation must allow
+#endif
+__global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
   State* st = p.st;
   __shared__ CycleSmem S;
   extern __shared__ double cdyn[];

@@ -85,16 +85,14 @@ def _upload(sysobj, jacobi: bool, stream):
         bt = b if isinstance(b, torch.Tensor) and b.is_cuda else torch.as_tensor(b).to("cuda")
         return A, bt, 0
     with torch.cuda.stream(stream):
-        dA = DeviceCsr.from_host(A, jacobi=False, non_blocking=True)
+        # the zero-pivot check is deferred (no sync on the upload stream)
+        dA = DeviceCsr.from_host(A, jacobi=jacobi, non_blocking=True, stream=stream,
+                                 check_pivot=False)
         if isinstance(b, torch.Tensor):
             bt = b.to("cuda", dtype=torch.float64, non_blocking=True)
         else:
             bt = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to("cuda")
         nb = _nbytes(dA.row_ptr) + _nbytes(dA.col_idx) + _nbytes(dA.values) + _nbytes(bt)
-        if jacobi:
-            from .sparse import _device_diagonal
-
-            dA = dA.with_diag(_device_diagonal(dA.n, dA.row_ptr, dA.col_idx, dA.values))
     return dA, bt, nb
 
 

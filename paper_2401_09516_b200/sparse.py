@@ -183,8 +183,14 @@ class DeviceCsr:
         return int(self.values.numel())
 
     @classmethod
-    def from_host(cls, A, jacobi: bool = False, device=None, stream=None, non_blocking=False):
-        """Upload a CsrMatrix-like (numpy or torch CPU arrays)."""
+    def from_host(cls, A, jacobi: bool = False, device=None, stream=None, non_blocking=False,
+                  check_pivot: bool = True):
+        """Upload a CsrMatrix-like (numpy or torch CPU arrays).
+
+        ``jacobi``: also keep the Jacobi diagonal; a zero pivot raises
+        ``ZeroPivotError`` (precond.py:153-158) here, which synchronises the
+        stream. ``check_pivot=False`` defers that check to
+        ``raise_if_zero_pivot()`` (one synchronisation for a whole batch)."""
         import torch
 
         dev = torch.device(device) if device is not None else torch.device("cuda")
@@ -207,19 +213,31 @@ class DeviceCsr:
             rp = _t(A.row_ptr, torch.int32)
             ci = _t(A.col_idx, torch.int32)
             vals = _t(A.values, torch.float64)
-            diag = None
-            if jacobi:
-                diag = _device_diagonal(n, rp, ci, vals)
-                if bool((diag == 0).any()):
-                    from .precond import ZeroPivotError
-
-                    zero = int(torch.nonzero(diag == 0)[0].item())
-                    raise ZeroPivotError("jacobi", zero)
-            dA = cls(n, rp, ci, vals, diag)
+            dA = cls(n, rp, ci, vals, None)
             off = stencil_offsets(A.row_ptr, A.col_idx) if stencil_enabled() else None
             if off is not None:
                 dA = dA.build_stencil(off, stream=stream)
+            if jacobi:
+                # the stencil build writes every row's diagonal entry into D
+                # (0 where a row has none), whether or not the form qualified
+                diag = (dA.stencil[0][64:64 + 8 * n].view(torch.float64)
+                        if dA.stencil is not None else _device_diagonal(n, rp, ci, vals))
+                dA = dA.with_diag(diag)
+                dA._pivot_flag = (diag == 0).any()
+                if check_pivot:
+                    dA.raise_if_zero_pivot()
         return dA
+
+    def raise_if_zero_pivot(self):
+        """ZeroPivotError for a zero Jacobi pivot (deferred check of from_host)."""
+        flag = getattr(self, "_pivot_flag", None)
+        if flag is not None and bool(flag):
+            import torch
+
+            from .precond import ZeroPivotError
+
+            zero = int(torch.nonzero(self.diag == 0)[0].item())
+            raise ZeroPivotError("jacobi", zero)
 
     def with_diag(self, diag):
         return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, diag, self._keep,

@@ -87,7 +87,11 @@ CONFIGS = {
     2: ConfigSpec(2, "helmholtz2d_256", "helmholtz", 2, 256, 1024, 3.0, 60, 20, "none",
                   max_iter=50000),
     3: ConfigSpec(3, "darcy3d_128", "darcy_binary", 3, 128, 512, 3.0, 40, 20, "jacobi"),
-    4: ConfigSpec(4, "darcy2d_1024", "darcy_binary", 2, 1024, 4096, 3.0, 40, 10, "jacobi"),
+    # C4: a cold start takes ~6,800 iterations and a poorly recycled system up
+    # to ~9,900 (measured), so the reference default 10,000 can bind: raised
+    # to 20,000 ("raise and state it if it is")
+    4: ConfigSpec(4, "darcy2d_1024", "darcy_binary", 2, 1024, 4096, 3.0, 40, 10, "jacobi",
+                  max_iter=20000),
 }
 
 

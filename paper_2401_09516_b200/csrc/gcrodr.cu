@@ -1157,34 +1157,27 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   const int mm = kc + j;
   if (defl) {
     // cross-Gram What[:, :mm]^T Vhat over this CTA's rows, register-tiled: a
-    // thread owns entries (ai + x*na4, bi + y*nb2), x < 4, y < 2, so
-    // consecutive lanes read consecutive columns of a 32-row tile staged
-    // column-major with an odd leading dimension (conflict-free). Per-CTA sums
-    // go to p.part[(GRAM_PART0 + entry) * GRID_MAX + blk]; after the barrier
-    // every entry is summed over the CTAs in a fixed order (deterministic).
-    // staged columns: [U (kc) | C (kc) | V_0..V_{j-1}]
+    // thread owns the 4 x 4 entries (ai + x*na4, bi + y*na4), so consecutive
+    // lanes read consecutive columns of a 32-row tile staged column-major with
+    // an odd leading dimension (conflict-free); 8 shared loads feed 16 FMAs.
+    // Per-CTA sums go to p.part[(GRAM_PART0 + entry) * GRID_MAX + blk]; after
+    // the barrier every entry is summed over the CTAs in a fixed order
+    // (deterministic). staged columns: [U (kc) | C (kc) | V_0..V_{j-1}]
     const int ncs = 2 * kc + j;
-    const int na4 = (mm + 3) / 4, nb2 = (mm + 1) / 2;
-    const int nblkt = na4 * nb2;  // thread blocks of entries
-    double gacc[2][8];
+    const int na4 = (mm + 3) / 4;
+    const int nblkt = na4 * na4;  // thread blocks of entries (<= 256 for mm <= 64)
+    double gacc[16];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) gacc[u][q] = 0.0;
-    int ca[2][4], cb[2][2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int tb = tid + u * NT;
-      int ai = tb % na4, bi = tb / na4;
+    for (int q = 0; q < 16; ++q) gacc[q] = 0.0;
+    int ca[4], cb[4];
+    {
+      const int ai = tid % na4, bi = tid / na4;
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         int a = min(ai + x * na4, mm - 1);
-        ca[u][x] = ((a < kc) ? kc + a : 2 * kc + (a - kc)) * GT_LD;  // What col: C or V
-      }
-#pragma unroll
-      for (int y = 0; y < 2; ++y) {
-        int b = min(bi + y * nb2, mm - 1);
-        cb[u][y] = ((b < kc) ? b : 2 * kc + (b - kc)) * GT_LD;  // Vhat col: U or V
+        ca[x] = ((a < kc) ? kc + a : 2 * kc + (a - kc)) * GT_LD;  // What col: C or V
+        int b = min(bi + x * na4, mm - 1);
+        cb[x] = ((b < kc) ? b : 2 * kc + (b - kc)) * GT_LD;  // Vhat col: U or V
       }
     }
     // the next 32-row tile is loaded into registers while this one is reduced
@@ -1217,40 +1210,32 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       __syncthreads();
       if (t0 + 32 < r1) load_tile(t0 + 32);
       __syncthreads();
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        int tb = tid + u * NT;
-        if (tb < nblkt) {
+      if (tid < nblkt) {
 #pragma unroll 4
-          for (int rrw = 0; rrw < 32; ++rrw) {
-            double wa[4], vb[2];
+        for (int rrw = 0; rrw < 32; ++rrw) {
+          double wa[4], vb[4];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) wa[x] = gtile[ca[u][x] + rrw];
+          for (int x = 0; x < 4; ++x) wa[x] = gtile[ca[x] + rrw];
 #pragma unroll
-            for (int y = 0; y < 2; ++y) vb[y] = gtile[cb[u][y] + rrw];
+          for (int y = 0; y < 4; ++y) vb[y] = gtile[cb[y] + rrw];
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
+          for (int x = 0; x < 4; ++x)
 #pragma unroll
-              for (int y = 0; y < 2; ++y) gacc[u][x * 2 + y] = fma(wa[x], vb[y], gacc[u][x * 2 + y]);
-          }
+            for (int y = 0; y < 4; ++y) gacc[x * 4 + y] = fma(wa[x], vb[y], gacc[x * 4 + y]);
         }
       }
       __syncthreads();
     }
+    if (tid < nblkt) {
+      const int ai = tid % na4, bi = tid / na4;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int tb = tid + u * NT;
-      if (tb < nblkt) {
-        int ai = tb % na4, bi = tb / na4;
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 2; ++y) {
-            int a = ai + x * na4, b = bi + y * nb2;
-            if (a < mm && b < mm)
-              p.part[(size_t)(GRAM_PART0 + a + b * mm) * GRID_MAX + blk] = gacc[u][x * 2 + y];
-          }
-      }
+        for (int y = 0; y < 4; ++y) {
+          const int a = ai + x * na4, b = bi + y * na4;
+          if (a < mm && b < mm)
+            p.part[(size_t)(GRAM_PART0 + a + b * mm) * GRID_MAX + blk] = gacc[x * 4 + y];
+        }
     }
   }
   {

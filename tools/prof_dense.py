@@ -16,7 +16,8 @@ systems = []
 for i in range(nsys):
     rp, ci, v, b, _ = P.assemble(spec, i)
     systems.append((skr.CsrMatrix(spec.N, spec.N, rp, ci, v), b))
-res = skr.solve_sequence(systems, list(range(nsys)), cfg, spec.precond, keep_x="none")
+res = skr.solve_sequence(systems, list(range(nsys)), cfg, spec.precond, keep_x="none",
+                         grid_ctas=int(os.environ.get("SKR_PROF_CTAS", "0")))
 eng = res.chain.engine
 L = _lib.load()
 prof = np.zeros(32, dtype=np.int64)

@@ -74,6 +74,10 @@ struct State {
   unsigned bar_pad0[62];             // alone on its 256-byte line
   unsigned bar_pad1[64];
   int* host_flag;  // mapped pinned: [0] = last processed cycle, [1] = done
+  // k_cycle neighbour epochs (stencil form): CTA b publishes at
+  // nb_epoch[b * NB_STRIDE] how many Arnoldi sweeps 2 it has finished in this
+  // solve; zeroed by k_init
+  unsigned nb_epoch[GRID_MAX * 16];
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
   int steps, pad2;    // Arnoldi steps executed
   long long prof[32]; // [0,16) dense-kernel phase clocks (recycle.h SKR_PHASE),
@@ -251,6 +255,7 @@ __global__ void __launch_bounds__(NT) k_init(Ptrs p, const double* x0) {
   }
   for (int v = threadIdx.x; v < 2 * KMAX; v += NT)
     p.part[(size_t)(COMB_PART0 + v) * GRID_MAX + blockIdx.x] = 0.0;
+  if (threadIdx.x == 0) p.st->nb_epoch[blockIdx.x * 16] = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -579,6 +584,7 @@ struct CycleSmem {
   double sc[16];             // scalars
   double bred[3 * NW];
   int flag;
+  unsigned ep;  // neighbour-epoch target of the current step
 };
 
 
@@ -777,6 +783,13 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   unsigned long long* bc = &st->bar_count;
   // completed grid barriers of this solve (no barrier is in flight at launch)
   unsigned long long bar_seen = tid == 0 ? ld_relaxed_gpu64(bc) / (unsigned long long)nblk : 0ull;
+  // Through the stencil form the next SpMV reads only rows within
+  // max(sx, sxy) of this CTA's own: after sweep 2 a CTA waits for the `halo`
+  // neighbour CTAs on each side instead of the whole grid.
+  unsigned* nbe = st->nb_epoch;
+  unsigned my_ep = tid == 0 ? ld_relaxed_gpu(nbe + blk * 16) : 0u;
+  const int halo = sten ? (max(p.sv.sx, p.sv.sxy) + p.rpb - 1) / p.rpb : -1;
+  const bool nbsync = halo >= 0 && 2 * halo + 1 < nblk && 2 * halo + 1 <= NT;
   int* abt = &st->abort_flag;
   // ---- cycle start --------------------------------------------------------
   const bool comb_part = st->comb_part != 0;
@@ -1129,7 +1142,45 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       break;
     }
     CPROF(3);
-    CYCLE_SYNC();
+    if (nbsync) {
+      // publish this CTA's sweep, then wait for the halo neighbours' (release /
+      // acquire at gpu scope, as grid_sync; a timeout aborts instead of hanging)
+      __syncthreads();
+      if (tid == 0) {
+        fence_acq_rel_gpu();
+        ++my_ep;
+        atomicExch(nbe + blk * 16, my_ep);
+        S.ep = my_ep;
+        S.flag = 0;
+      }
+      __syncthreads();
+      const int nb = blk - halo + tid;
+      if (tid <= 2 * halo && nb >= 0 && nb < nblk && nb != blk) {
+        const unsigned target = S.ep;
+        unsigned long long t0 = gtimer();
+        unsigned polls = 0;
+        while (ld_acquire_gpu(nbe + nb * 16) < target) {
+          if ((++polls & 255) == 0 &&
+              (gtimer() - t0 > BARRIER_TIMEOUT_NS ||
+               ld_relaxed_gpu(reinterpret_cast<unsigned*>(abt)))) {
+            atomicExch(abt, 1);
+            S.flag = 1;
+            break;
+          }
+        }
+        fence_acq_rel_gpu();
+      }
+      __syncthreads();
+      if (S.flag) {
+        if (tid == 0) {
+          st->done = 1;
+          if (blk == 0) flag_host(st, cycle_id, 1);
+        }
+        return;
+      }
+    } else {
+      CYCLE_SYNC();
+    }
     CPROF(4);
   }
 

@@ -1217,12 +1217,19 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     const int ncs = 2 * kc + j;
     const int na4 = (mm + 3) / 4;
     const int nblkt = na4 * na4;  // thread blocks of entries (<= 256 for mm <= 64)
+    // G groups of threads split each tile's 32 rows (idle threads otherwise);
+    // their sums are added in group order through the staging area at the end
+    int ngr = NT / nblkt;
+    ngr = ngr > 4 ? 4 : ngr;
+    while (ngr > 1 && (size_t)(ngr - 1) * nblkt * 16 > (size_t)p.sm_R) --ngr;
+    const int gblk = tid % nblkt, grp = tid / nblkt;
+    const int rows_g = 32 / ngr, rlo = grp * rows_g, rhi = grp == ngr - 1 ? 32 : rlo + rows_g;
     double gacc[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) gacc[q] = 0.0;
     int ca[4], cb[4];
     {
-      const int ai = tid % na4, bi = tid / na4;
+      const int ai = gblk % na4, bi = gblk / na4;
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         int a = min(ai + x * na4, mm - 1);
@@ -1261,9 +1268,9 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       __syncthreads();
       if (t0 + 32 < r1) load_tile(t0 + 32);
       __syncthreads();
-      if (tid < nblkt) {
+      if (grp < ngr) {
 #pragma unroll 4
-        for (int rrw = 0; rrw < 32; ++rrw) {
+        for (int rrw = rlo; rrw < rhi; ++rrw) {
           double wa[4], vb[4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) wa[x] = gtile[ca[x] + rrw];
@@ -1277,8 +1284,18 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       }
       __syncthreads();
     }
-    if (tid < nblkt) {
-      const int ai = tid % na4, bi = tid / na4;
+    if (ngr > 1) {  // groups 1.. hand their sums to group 0 (fixed order)
+      if (grp >= 1 && grp < ngr)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) gtile[((size_t)(grp - 1) * nblkt + gblk) * 16 + q] = gacc[q];
+      __syncthreads();
+      if (grp == 0)
+        for (int g = 1; g < ngr; ++g)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) gacc[q] += gtile[((size_t)(g - 1) * nblkt + gblk) * 16 + q];
+    }
+    if (grp == 0) {
+      const int ai = gblk % na4, bi = gblk / na4;
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll

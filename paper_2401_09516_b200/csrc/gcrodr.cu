@@ -849,6 +849,9 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         row[i] = ok[i] ? rr : r1 - 1;
         w[i] = Vt[row[i]];
       }
+      double dgv[R];  // Jacobi pivots, loaded ahead of the SpMV's dependent chain
+#pragma unroll
+      for (int i = 0; i < R; ++i) dgv[i] = p.dg ? __ldg(p.dg + row[i]) : 1.0;
       if (do_spmv) {
         if (sten_local) {
 #pragma unroll
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
           spmv_rows<R, false>(p.rp, p.ci, p.av, Vt, row, ok, r0, z);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          if (p.dg) z[i] = __ddiv_rn(z[i], __ldg(p.dg + row[i]));
+          if (p.dg) z[i] = __ddiv_rn(z[i], dgv[i]);
           if (ok[i]) p.z[row[i]] = z[i];
         }
       } else {
@@ -1065,12 +1068,16 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         const int tile = ntile - 1 - rt;
         const int base = r0 + tile * TR + lane;
         bool ok[R];
-        double ta[R], tb[R];
+        double ta[R], tb[R], wv[R], zv[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           ok[i] = base + 32 * i < r1;
           ta[i] = 0.0;
           tb[i] = 0.0;
+          // this row's pending vector and z, in flight during the batches
+          const int rr = ok[i] ? base + 32 * i : r1 - 1;
+          wv[i] = Vt[rr];
+          zv[i] = p.z[rr];
         }
         if (need) {
           for (int c0 = 0; c0 < pb; c0 += SW2_COLS) {
@@ -1098,13 +1105,12 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         for (int i = 0; i < R; ++i) {
           if (!ok[i]) continue;
           const int rr = base + 32 * i;
-          const double wv = Vt[rr], zv = p.z[rr];
-          double vt = wv;
+          double vt = wv[i];
           if (t >= 1) {
-            vt = brk ? 0.0 : (wv - ta[i]) / eta;
+            vt = brk ? 0.0 : (wv[i] - ta[i]) / eta;
             Vt[rr] = vt;
           }
-          if (!stop) Vn[rr] = (zv - tb[i]) / eta - vt * htt;  // tb: unscaled b
+          if (!stop) Vn[rr] = (zv[i] - tb[i]) / eta - vt * htt;  // tb: unscaled b
         }
       }
 

@@ -1060,6 +1060,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     // ---- sweep 2: finish V_t, project the new vector into V_{t+1} ----------
     {
       const double htt = S.sc[3];
+      const double ieta = 1.0 / eta;  // one reciprocal per step, not two divides per row
       double* Vn = colV(p, t + 1);
       const bool need = (t >= 1 || !stop);
       // tiles in the reverse order of sweep 1 (and of the next sweep 1): the
@@ -1107,10 +1108,10 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
           const int rr = base + 32 * i;
           double vt = wv[i];
           if (t >= 1) {
-            vt = brk ? 0.0 : (wv[i] - ta[i]) / eta;
+            vt = brk ? 0.0 : (wv[i] - ta[i]) * ieta;
             Vt[rr] = vt;
           }
-          if (!stop) Vn[rr] = (zv[i] - tb[i]) / eta - vt * htt;  // tb: unscaled b
+          if (!stop) Vn[rr] = (zv[i] - tb[i]) * ieta - vt * htt;  // tb: unscaled b
         }
       }
 

@@ -584,6 +584,7 @@ struct CycleSmem {
   double sc[16];             // scalars
   double bred[3 * NW];
   int flag;
+  unsigned ep;  // neighbour-epoch target of the current step
 };
 
 

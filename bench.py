@@ -288,10 +288,15 @@ def run_skr(args):
     # ---- this rank's chunk of the chain ------------------------------------
     chunk = skr.chunk_positions(spec.n_systems, world, rank)
     need = (W + K) * S
-    if len(chunk) < need:
-        raise SystemExit(f"rank {rank}: chunk of {len(chunk)} systems < {need} needed "
-                         f"(warmup+steps)*stripe; raise --n-systems or lower --stripe")
-    pos = list(chunk)[:need]
+    chunk = list(chunk)
+    if not chunk:
+        raise SystemExit(f"rank {rank}: empty chunk")
+    # a rank's chunk (n_systems / world) can be shorter than the (W + K) * S
+    # systems a long run needs (e.g. 8 GPUs, many steps): the chains then
+    # continue through the chunk again (every solve is real work; the jump
+    # back costs one poorly recycled system per chain)
+    wrapped = len(chunk) < need
+    pos = [chunk[i % len(chunk)] for i in range(need)]
     idxs = [order[p] for p in pos]
     host = []
     for i in idxs:
@@ -464,7 +469,7 @@ def run_skr(args):
         "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator; DCT-sampled GRF, see DESIGN.md)",
-        "config": dict(_config_dict(spec, S, world), chains_per_gpu=NC,
+        "config": dict(_config_dict(spec, S, world), chains_per_gpu=NC, chunk_wrapped=wrapped,
                        ctas_per_chain=gctas,
                        l2=("flushed between steps (256 MiB write)" if args.sync_steps else
                            "flushed (256 MiB write) before the timed region; inside it each "
@@ -481,9 +486,11 @@ def run_skr(args):
                      "per_launch_gbs": per_launch, "aggregate_gbs": aggregate,
                      "kernel": "k_cycle (persistent DCGS2 Arnoldi cycle: SpMV + ortho)",
                      "peak_source": peak_src,
-                     "algorithmic_bytes": "per step B_spmv + 8N(2p+6), SURVEY 8(d)",
-                     "note": "C1 working set (~39 MB) is L2-resident: achieved may be "
-                             "L2-bandwidth/latency-bound rather than HBM-bound"},
+                     "algorithmic_bytes": ("per step B_spmv + 8N(2p+6), SURVEY 8(d); B_spmv = 24N + 16N "
+                                           "through the stencil form (2-D), 12 nnz + 4(N+1) + 16N "
+                                           "through the CSR"),
+                     "note": "one chain's C1 working set (~39 MB) fits the L2; the 8 concurrent "
+                             "chains' (~312 MB) do not"},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -21,7 +21,7 @@ for i in range(ns):
 torch.cuda.synchronize()
 chunks = skr.split_chunks(list(range(ns)), nch)
 res = skr.solve_chains(systems, list(range(ns)), cfg, spec.precond, chunks, keep_x="none",
-                       grid_ctas=skr.chain_grid_ctas(nch))
+                       grid_ctas=int(os.environ.get("PROBE_CTAS", "0")) or skr.chain_grid_ctas(nch))
 for ch, r in zip(chunks, res):
     print("chunk", ch, "iters", r.iterations, "conv", r.converged, "true_rel",
           [f"{v:.2e}" for v in r.true_rel], "warn", r.warn_bits)

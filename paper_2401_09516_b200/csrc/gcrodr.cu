@@ -959,19 +959,30 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     const double* A_ = S.red + 3;
     const double* BB = S.red + 3 + pb;
     if (warp == 0) {
-      double aa = 0.0, ab = 0.0, cc = 0.0;
+      double aa = 0.0, ab = 0.0, cc = 0.0, ag = 0.0;
       for (int c = lane; c < pb; c += 32) {
         double av = (t >= 1) ? A_[c] : 0.0, bv = BB[c];
         aa += av * av;
         ab += av * bv;
-        if (c < kc) cc += bv * bv;
+        if (c < kc) {
+          cc += bv * bv;
+          ag += av * S.cr[c];  // a_C . (C^T r)
+        }
       }
       for (int o = 16; o > 0; o >>= 1) {
         aa += __shfl_xor_sync(0xffffffffu, aa, o);
         ab += __shfl_xor_sync(0xffffffffu, ab, o);
         cc += __shfl_xor_sync(0xffffffffu, cc, o);
+        ag += __shfl_xor_sync(0xffffffffu, ag, o);
       }
-      const double eta0 = (t >= 1) ? sqrt(fmax(S.red[0] - aa, 0.0)) : 1.0;
+      // ||w - Q a||^2 = ||w||^2 - |a|^2 + a^T (Q^T Q - I) a. Every basis
+      // vector is projected against C except V_0 = r / beta (reference
+      // semantics), whose Gram block with C is C^T r / beta (the cycle-start
+      // c_r): near convergence r's direction is rounding noise, V_0 is far
+      // from orthogonal to C, and without this term the Pythagorean eta falls
+      // to 0 (a spurious breakdown; the reference measures ||w|| directly).
+      const double gcorr = (t >= 1 && kc > 0) ? 2.0 * A_[kc] * ag / beta : 0.0;
+      const double eta0 = (t >= 1) ? sqrt(fmax(S.red[0] - aa + gcorr, 0.0)) : 1.0;
       const bool brk0 =
           t >= 1 && eta0 < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308);
       if (t >= 1) {

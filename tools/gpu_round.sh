@@ -1,7 +1,7 @@
 # Evidence pass (part A): parity tests, default bench, ncu launch list of a
 # short bench (one ncu per call; part B = tools/gpu_round_b.sh).
 set -o pipefail
-TAG=${TAG:-r01f}
+TAG=${TAG:-r01g}
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo pytest_rc=$?
 tail -2 gpurun_out/pytest_gpu_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo bench_rc=$?

@@ -81,7 +81,7 @@ typedef struct skr_report {
   int32_t zero_rhs;       /* b == 0 early return (gcrodr.py:337-346) */
   int32_t gmres_fallback; /* U stayed None (gcrodr.py:481-483) */
   int32_t cycles;
-  int32_t reserved;
+  int32_t v0_projections; /* cycles whose V_0 was formed from r - C C^T r */
   double true_relative_residual;
   double rnorm;
   double abs_tol;

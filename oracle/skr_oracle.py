@@ -416,7 +416,7 @@ class Result:
     info: dict = field(default_factory=dict)
 
 
-def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None) -> Result:
+def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None) -> Result:
     """GCRO-DR solve with a carried recycle basis (gcrodr.py:295-496).
 
     ``U_in`` is the previous system's recycle U (its C is discarded by the
@@ -477,6 +477,8 @@ def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None) -> Result:
         Ut = U * dk
         cr = C.T @ r
         beta = rnorm
+        if trace is not None:  # diagnostics: |C^T r| / beta at every cycle start
+            trace.append((iters, beta, float(np.linalg.norm(cr)) / beta))
         V = np.zeros((n, nsteps + 1))
         H = np.zeros((nsteps + 1, nsteps))
         B = np.zeros((kc, nsteps))

@@ -49,7 +49,7 @@ class SkrReport(ctypes.Structure):
     _fields_ = [("iterations", c_int32), ("converged", c_int32), ("k_out", c_int32),
                 ("hist_len", c_int32), ("n_checks", c_int32), ("deflated_steps", c_int32),
                 ("warn_bits", c_int32), ("status_bits", c_int32), ("zero_rhs", c_int32),
-                ("gmres_fallback", c_int32), ("cycles", c_int32), ("reserved", c_int32),
+                ("gmres_fallback", c_int32), ("cycles", c_int32), ("v0_projections", c_int32),
                 ("true_relative_residual", c_double), ("rnorm", c_double),
                 ("abs_tol", c_double), ("bnorm", c_double), ("device_ms", c_double),
                 ("spmv_ortho_bytes", c_double), ("cycle_kernel_ms", c_double),

@@ -79,7 +79,7 @@ struct State {
   // solve; zeroed by k_init
   unsigned nb_epoch[GRID_MAX * 16];
   double step_bytes;  // algorithmic SpMV+ortho bytes accumulated
-  int steps, pad2;    // Arnoldi steps executed
+  int steps, v0proj;  // Arnoldi steps executed; cycles whose V_0 was formed from r - C c_r
   long long prof[32]; // [0,16) dense-kernel phase clocks (recycle.h SKR_PHASE),
                       // [16,24) k_cycle phase clocks of CTA 0
   int kept[KMAX];
@@ -668,6 +668,9 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
     }                                                             \
   } while (0)
 
+// |C^T r| / beta above which the cycle forms V_0 from r - C C^T r (cycle start)
+constexpr double V0_PROJ_RTOL = 1e-6;
+
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
 
 // k_cycle dynamic shared memory, sized by (m, kcap) (offsets in doubles):
@@ -803,15 +806,61 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       S.cr[tid] = S.red[tid];
     }
   }
-  if (tid == 0) S.gv[0] = beta;
+  // V_0. The reference takes r / beta as it is (gcrodr.py:412). In exact
+  // arithmetic C^T r = 0 at every cycle start (the refresh projection and the
+  // deflated LS both leave r orthogonal to C), but in floating point the
+  // reference's cycle does not remove a C-component of r: its LS right-hand
+  // side [c_r; beta; 0] counts c_r once more than r = beta V_0 holds it, so
+  // the component comes back with flipped sign and grows through the C^T V
+  // Gram terms (measured: |c_r| / beta x2-4 per cycle on some C3 systems,
+  // up to 0.4, then the residual stalls at |c_r| and DCGS2's Pythagorean norm
+  // reports a spurious breakdown). When |c_r| > V0_PROJ_RTOL beta, V_0 is
+  // therefore formed from r - C c_r with its measured norm beta0 (r =
+  // C c_r + beta0 V_0 exactly, [C | V] orthonormal again); the LS keeps the
+  // reference's form [c_r; beta0; 0]. Equal in exact arithmetic (c_r = 0).
+  double beta0 = beta;
+  bool v0proj = false;
+  if (defl) {
+    __syncthreads();
+    double c2 = 0.0;
+    for (int q = 0; q < kc; ++q) c2 = fma(S.cr[q], S.cr[q], c2);  // same order in every CTA
+    v0proj = c2 > (V0_PROJ_RTOL * beta) * (V0_PROJ_RTOL * beta);
+  }
   {
     double* V0 = colV(p, 0);
-    for (int row = r0 + tid; row < r1; row += NT) V0[row] = p.r[row] / beta;
+    if (v0proj) {
+      double ss = 0.0;
+      for (int row = r0 + tid; row < r1; row += NT) {
+        double v = p.r[row];
+        for (int c = 0; c < kc; ++c) v = fma(-colC(p, kcap - kc + c)[row], S.cr[c], v);
+        V0[row] = v;
+        ss = fma(v, v, ss);
+      }
+      const double t_ss = block_sum(ss, S.bred);
+      if (tid == 0) p.part[(size_t)GRAM_PART0 * GRID_MAX + blk] = t_ss;
+      CYCLE_SYNC();
+      reduce_partials(p.part + (size_t)GRAM_PART0 * GRID_MAX, GRID_MAX, nblk, 0, 1, S.red);
+      beta0 = sqrt(S.red[0]);
+      for (int row = r0 + tid; row < r1; row += NT) V0[row] = V0[row] / beta0;
+      if (blk == 0 && tid == 0) st->v0proj += 1;
+    } else {
+      for (int row = r0 + tid; row < r1; row += NT) V0[row] = p.r[row] / beta;
+    }
   }
+  if (tid == 0) S.gv[0] = beta0;
   if (blk == 0 && tid < kc) {
     st->dk[tid] = S.dk[tid];
     st->cr[tid] = S.cr[tid];
   }
+#ifdef SKR_DIAG
+  __syncthreads();
+  if (blk == 0 && tid == 0) {
+    double c2 = 0.0;
+    for (int q = 0; q < kc; ++q) c2 += S.cr[q] * S.cr[q];
+    printf("DIAG start st=%p cyc=%d kc=%d iters=%d beta=%.3e abstol=%.3e cr/beta=%.3e\n", (void*)st,
+           st->cycles, kc, st->iters, beta, abs_tol, sqrt(c2) / beta);
+  }
+#endif
   if (blk == 0)
     for (int v = tid; v < 3 * PV_STEP; v += NT) st->acc[(size_t)v * ACC_STRIDE] = 0.0;
   int red_idx = 0;
@@ -823,7 +872,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   int j = 0;
   bool brk = false;
   double wn0_pending = 0.0;  // ||w - C C^T w|| / eta of the pending vector's step
-  double hres = beta;
+  double hres = beta0;
   long long cprof_t = clock64();
   for (int t = 0; t <= s; ++t) {
     const bool do_spmv = (t < s);
@@ -981,10 +1030,15 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       // c_r): near convergence r's direction is rounding noise, V_0 is far
       // from orthogonal to C, and without this term the Pythagorean eta falls
       // to 0 (a spurious breakdown; the reference measures ||w|| directly).
-      const double gcorr = (t >= 1 && kc > 0) ? 2.0 * A_[kc] * ag / beta : 0.0;
+      const double gcorr = (t >= 1 && kc > 0 && !v0proj) ? 2.0 * A_[kc] * ag / beta : 0.0;
       const double eta0 = (t >= 1) ? sqrt(fmax(S.red[0] - aa + gcorr, 0.0)) : 1.0;
       const bool brk0 =
           t >= 1 && eta0 < 1e-14 * fmax(wn0_pending, 2.2250738585072014e-308);
+#ifdef SKR_DIAG
+      if (blk == 0 && lane == 0 && t >= 1 && (brk0 || S.red[0] - aa + gcorr < 0.5 * S.red[0]))
+        printf("DIAG bessel st=%p cyc=%d t=%d nu=%.3e aa=%.3e gcorr=%.3e eta0=%.3e wn0=%.3e brk=%d\n",
+               (void*)st, st->cycles, t, S.red[0], aa, gcorr, eta0, wn0_pending, (int)brk0);
+#endif
       if (t >= 1) {
         // final column i = t-1: first pass + reorthogonalisation coefficients
         const int i = t - 1;
@@ -1352,6 +1406,10 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       double rnorm = sqrt(S.red[0]);
       st->rnorm = rnorm;
       st->converged = rnorm <= abs_tol ? 1 : 0;
+#ifdef SKR_DIAG
+      printf("DIAG end st=%p cyc=%d j=%d brk=%d lsres=%.3e rnorm=%.3e conv=%d\n", (void*)st, st->cycles,
+             j, st->brk, st->g[0], rnorm, st->converged);
+#endif
       p.checks[2 * st->nchecks] = st->g[0];
       p.checks[2 * st->nchecks + 1] = rnorm;
       st->nchecks += 1;
@@ -1666,6 +1724,12 @@ __global__ void __launch_bounds__(NT) k_sten_upper(int n, const int32_t* rp, con
       const int d = __ldg(ci + q) - i;
       if (d <= 0) continue;
       const double v = __ldg(av + q);
+      // only the three upper diagonals have a mirror array (B only in 3-D);
+      // any other positive offset disqualifies the row without a load
+      if (d != 1 && d != sv.sx && !(sv.sxy && d == sv.sxy)) {
+        bad = true;
+        continue;
+      }
       const double m = d == 1 ? sv.W[i + 1] : d == sv.sx ? sv.S[i + sv.sx] : sv.B[i + sv.sxy];
       if (v == 0.0 || __double_as_longlong(v) != __double_as_longlong(m)) bad = true;
       ++nup;
@@ -2177,6 +2241,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   rep->zero_rhs = hs.zero_rhs;
   rep->gmres_fallback = hs.kc == 0 ? 1 : 0;
   rep->cycles = hs.cycles;
+  rep->v0_projections = hs.v0proj;
   rep->true_relative_residual = hs.true_rel;
   rep->rnorm = hs.rnorm;
   rep->abs_tol = hs.abs_tol;

@@ -52,6 +52,7 @@ class SequenceResult:
     device_ms: list = field(default_factory=list)
     k_out: list = field(default_factory=list)
     warn_bits: list = field(default_factory=list)
+    v0_projections: list = field(default_factory=list)
     spmv_ortho_bytes: float = 0.0
     x: list = field(default_factory=list)
     launches: int = 0
@@ -156,6 +157,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
         res.device_ms.append(float(rep.device_ms))
         res.k_out.append(int(rep.k_out))
         res.warn_bits.append(int(rep.warn_bits))
+        res.v0_projections.append(int(rep.v0_projections))
         res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
         res.launches += int(rep.launches)
         res.cycle_kernel_ms += float(rep.cycle_kernel_ms)
@@ -336,6 +338,7 @@ def _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states, g
             res.device_ms.append(float(rep.device_ms))
             res.k_out.append(int(rep.k_out))
             res.warn_bits.append(int(rep.warn_bits))
+            res.v0_projections.append(int(rep.v0_projections))
             res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
             res.launches += int(rep.launches)
             res.cycle_kernel_ms += float(rep.cycle_kernel_ms)

@@ -140,6 +140,15 @@ def test_stencil_rejects_non_stencil_matrices():
     rp4 = rp.copy()
     rp4[r + 1:] -= 1
     check(rp4, ci[keep], v[keep], False)
+    # row 0 looks like a 2-D 5-point row, but a later row has a symmetric pair
+    # at offset +-2 (no mirror array exists for it in 2-D: the build must
+    # reject the matrix without touching the absent 3-D plane)
+    S = A.to_scipy().tolil()
+    S[r, r + 2] = -0.25
+    S[r + 2, r] = -0.25
+    S = S.tocsr()
+    S.sort_indices()
+    check(S.indptr.astype(np.int64), S.indices.astype(np.int64), S.data.copy(), False)
 
 
 @pytest.mark.parametrize("cid,n", [(0, None), (1, 40), (2, 24), (3, 10), (4, 64)])

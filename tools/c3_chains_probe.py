@@ -24,4 +24,4 @@ res = skr.solve_chains(systems, list(range(ns)), cfg, spec.precond, chunks, keep
                        grid_ctas=int(os.environ.get("PROBE_CTAS", "0")) or skr.chain_grid_ctas(nch))
 for ch, r in zip(chunks, res):
     print("chunk", ch, "iters", r.iterations, "conv", r.converged, "true_rel",
-          [f"{v:.2e}" for v in r.true_rel], "warn", r.warn_bits)
+          [f"{v:.2e}" for v in r.true_rel], "warn", r.warn_bits, "v0proj", r.v0_projections)

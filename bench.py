@@ -1,22 +1,34 @@
 #!/usr/bin/env python
 """SKR hot-path benchmark: systems solved/s (rel-res 1e-8, fp64) on B200.
 
-Workload (BASELINE.json configs[1]): variable-coefficient Poisson on 256^2
-(N = 65,536), a batch of 1,024 systems, greedy-NN sorted on the coefficient
-field, solved as GCRO-DR(40, 10) chains with Jacobi. The sorted order is
-split into contiguous per-GPU chunks (one recycling chain per rank, weak
-scaling). A bench *step* = one stripe of S consecutive systems of the
-rank's chain; the chain (and its recycle space) continues across steps.
+Workload (default BASELINE.json configs[3], "C3"): 3-D Darcy flow on a 128^3
+grid (N = 2,097,152, 7-point FD, ~14.6 M nonzeros), a batch of 512 systems
+with a in {3, 12} from a thresholded GRF, greedy-NN sorted on a, solved as
+GCRO-DR(40, 20) chains with Jacobi, tol 1e-8. C3 is the largest single-GPU
+configuration whose working set (1.6 GB per chain) is far beyond the 126 MB
+L2, i.e. the HBM-gated one of SURVEY 8(d). ``--config 1`` etc. select the
+other configurations.
 
-* value  : device-resident inputs (CSR + b already in HBM), timed with CUDA
-           events, L2 flushed between steps, max over ranks.
-* e2e    : the same stripes through the public API with pinned host CSR/b
-           uploaded (H2D) and x read back (D2H) inside every step.
-* roofline: SURVEY 8(d) algorithmic SpMV+ortho bytes / summed CUDA-event time
-           of the Arnoldi-cycle kernel launches, vs MEASURED_PEAKS.json HBM.
-* cpu_baseline: the oracle port (numpy/scipy = the reference's arithmetic) on
-           this host's cores, on a bounded sample of the same chain.
+The sorted order is split into contiguous per-GPU chunks (one set of
+recycling chains per rank, weak scaling, no collective on the solve path).
+Inside a GPU the chunk is split again into ``--chains`` concurrent chains
+(each on its own stream with a share of the SMs). A bench *step* = one
+stripe of S consecutive systems (S / chains per chain); the chains (and their
+recycle spaces) continue across steps.
+
+* value  : device-resident inputs (CSR + stencil form + b already in HBM),
+           K stripes timed with CUDA events, barrier + synchronize on both
+           sides, max over ranks.
+* e2e    : the same stripes through the public API with the pinned host
+           CSR/b uploaded (H2D) and x read back (D2H) inside the timed region.
+* roofline: SURVEY 8(d) algorithmic SpMV+ortho bytes of the k_cycle launches
+           over the timed region (concurrent chains), vs MEASURED_PEAKS.json
+           HBM and vs the nominal 8 TB/s.
+* cpu_baseline: the oracle port (numpy/scipy: the reference's arithmetic) on
+           this host's cores, on a bounded sample (extrapolated, see below).
 ``--impl reference`` runs the reference's CPU path (oracle port) on rank 0.
+``--gpus N`` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks.
 """
 
 from __future__ import annotations
@@ -39,6 +51,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "linear systems solved/sec to rel-res 1e-8 (fp64)"
+NOMINAL_HBM_GBS = 8000.0  # BASELINE.json: "SpMV+ortho HBM GB/s vs 8 TB/s"
+
+# per-config defaults: (chains per GPU, systems per step). Measured on B200
+# (tools/gpu_sweep_c3.sh): C3 8 chains 5.75 systems/s, 4: 5.68, 2: 5.49,
+# 1: 5.17; C4 8: 1.05, 1: 0.94; C1 8 x 64 CTAs.
+DEFAULTS = {0: (8, 16), 1: (8, 16), 2: (8, 8), 3: (8, 8), 4: (8, 8)}
 
 
 def _args():
@@ -47,9 +65,9 @@ def _args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="skr", choices=["skr", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--stripe", type=int, default=16, help="systems per step")
-    ap.add_argument("--chains", type=int, default=8,
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--stripe", type=int, default=None, help="systems per step")
+    ap.add_argument("--chains", type=int, default=None,
                     help="independent recycling chains per GPU (contiguous sub-chunks)")
     ap.add_argument("--ctas-per-chain", type=int, default=None,
                     help="CTAs of each chain's Arnoldi kernel (default: chain_grid_ctas)")
@@ -59,8 +77,31 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sync-steps", action="store_true",
                     help="time each stripe separately (L2 flush + barrier between stripes)")
-    ap.add_argument("--cpu-budget-s", type=float, default=25.0)
-    return ap.parse_args()
+    ap.add_argument("--cpu-budget-s", type=float, default=25.0,
+                    help="CPU seconds of the GPU arm's cpu_baseline sample")
+    ap.add_argument("--ref-step-s", type=float, default=25.0,
+                    help="CPU seconds per step of the --impl reference arm")
+    a = ap.parse_args()
+    ch, st = DEFAULTS.get(a.config, (8, 16))
+    a.chains = ch if a.chains is None else a.chains
+    a.stripe = st if a.stripe is None else a.stripe
+    return a
+
+
+def _relaunch_under_torchrun(args) -> int | None:
+    """``--gpus N`` (N > 1) from a plain ``python bench.py``: run N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def _dist():
@@ -92,9 +133,31 @@ def _spec(args):
 
 
 def _params(spec):
+    """All systems' sort parameters (n_sys x P fp64), generated in parallel."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from paper_2401_09516_b200 import problems as P
 
-    return np.stack([P.system_params(spec, i)["params"] for i in range(spec.n_systems)])
+    first = P.system_params(spec, 0)["params"]
+    flat = np.empty((spec.n_systems, first.size), dtype=np.float64)
+    flat[0] = first
+
+    def fill(i):
+        flat[i] = P.system_params(spec, i)["params"]
+
+    with ThreadPoolExecutor(max_workers=max(1, min(16, _CORES))) as ex:
+        list(ex.map(fill, range(1, spec.n_systems)))
+    return flat
+
+
+def _fields(spec, i, flat):
+    """Generator fields of system i (the sort row is the coefficient field
+    itself for the Darcy / Poisson kinds: no second GRF draw)."""
+    from paper_2401_09516_b200 import problems as P
+
+    if spec.kind in ("darcy_binary", "poisson_lognormal"):
+        return {"a": flat[i].reshape((spec.n,) * spec.dim), "params": flat[i]}
+    return P.system_params(spec, i)
 
 
 def _peaks():
@@ -107,13 +170,15 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic():
-    """dram bytes per k_cycle launch from the committed ncu --set full summary."""
+def _traffic(cid):
+    """DRAM bytes / algorithmic bytes of k_cycle from the committed ncu
+    --set full capture of this configuration's bench shape (profiles/)."""
     path = os.path.join(ROOT, "profiles", "ncu_k_cycle_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+        d = d.get(f"C{cid}", d)
+        return d.get("dram_over_algorithmic"), d.get("source")
     except Exception:
         return None, None
 
@@ -170,57 +235,6 @@ def _flush_l2(buf):
     buf.add_(1.0)
 
 
-def run_reference(args):
-    """The reference's CPU path (oracle port of kryrec) on rank 0's host cores."""
-    world, rank, _ = _dist_cpu()
-    if rank != 0:
-        return
-    from oracle import skr_oracle as orc
-    from paper_2401_09516_b200 import problems as P
-
-    spec = _spec(args)
-    t0 = time.perf_counter()
-    flat = _params(spec)
-    npos = args.warmup + args.steps
-    order = orc.greedy_order_prefix(flat, npos)
-    prefix_sort_s = time.perf_counter() - t0
-    cfg = orc.Cfg(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
-    U = None
-    walls, its = [], []
-    for pos in range(npos):
-        rp, ci, v, b, _ = P.assemble(spec, order[pos])
-        op = orc.Operator(rp, ci, v, spec.N, spec.precond == "jacobi")
-        r = orc.gcrodr(op, b, cfg, U_in=U)
-        U = r.U
-        if pos >= args.warmup:
-            walls.append(r.wall_time)
-            its.append(r.iterations)
-    total = sum(walls)
-    value = len(walls) / total
-    out = {
-        "metric": METRIC, "value": value, "unit": "systems/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(walls),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded config generator)", "impl": "reference",
-        "config": _config_dict(spec, 1, world),
-        "cpu_baseline": {"value": value, "unit": "systems/s", "cores": _CORES, "kind": "port",
-                         "sample": f"oracle chain positions {args.warmup}..{npos - 1} of the "
-                                   f"sorted order, one system per step (prefix sort "
-                                   f"{prefix_sort_s:.1f}s excluded)"},
-        "e2e": {"value": value, "unit": "systems/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-        "iterations_mean": float(np.mean(its)),
-        "cpu_model": _cpu_model(),
-    }
-    print(json.dumps(out), flush=True)
-
-
-def _dist_cpu():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    return world, rank, 0
-
-
 def _cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -232,27 +246,120 @@ def _cpu_model():
     return None
 
 
-def _config_dict(spec, stripe, world):
+def _reference_iters_per_system(cid):
+    """The reference's own iterations per recycled system of this config, from
+    the committed kryrec run (tests/golden/full_c<cid>.npz, positions >= 1)."""
+    path = os.path.join(ROOT, "tests", "golden", f"full_c{cid}.npz")
+    try:
+        g = np.load(path)
+        it = np.asarray(g["iters"], dtype=float)
+        rec = it[1:] if it.size > 1 else it
+        return float(rec.mean()), f"kryrec chain, tests/golden/full_c{cid}.npz ({rec.size} systems)"
+    except Exception:
+        return None, None
+
+
+def _oracle_sample(spec, systems, step_s, U_in=None):
+    """The oracle (reference arithmetic) GCRO-DR chain over ``systems`` (a list
+    of (row_ptr, col_idx, values, b)), each solve bounded to ``step_s`` CPU
+    seconds: a solve still running then stops at its next cycle boundary (a
+    real partial solve through the reference's code path; its recycle space is
+    carried on, as the reference carries an unconverged solve's). Returns the
+    (iterations, wall seconds, converged) per system and the last recycle U."""
+    from oracle import skr_oracle as orc
+
+    out = []
+    U = U_in
+    cfg = orc.Cfg(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
+    for rp, ci, v, b in systems:
+        op = orc.Operator(rp, ci, v, spec.N, spec.precond == "jacobi")
+        r = orc.gcrodr(op, b, cfg, U_in=U, deadline=time.perf_counter() + step_s)
+        U = r.U if r.U is not None else U
+        out.append((int(r.iterations), float(r.wall_time), bool(r.converged)))
+    return out, U
+
+
+def _cpu_rate(samples, iters_per_system):
+    """systems/s of the CPU path: whole systems when every sampled solve
+    converged, else its iterations/s divided by the iterations per system."""
+    if samples and all(s[2] for s in samples):
+        return len(samples) / sum(s[1] for s in samples), "measured (whole systems)"
+    its = sum(s[0] for s in samples)
+    wall = sum(s[1] for s in samples)
+    return (its / wall) / iters_per_system, "extrapolated from iterations/s"
+
+
+def run_reference(args):
+    """The reference's CPU path (oracle port of kryrec: the reference is pure
+    Python and cannot travel to the GPU box) on rank 0's host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import skr_oracle as orc
+    from paper_2401_09516_b200 import problems as P
+
+    spec = _spec(args)
+    t0 = time.perf_counter()
+    flat = _params(spec)
+    npos = args.warmup + args.steps
+    order = orc.greedy_order_prefix(flat, npos + 1)
+    prefix_sort_s = time.perf_counter() - t0
+    ref_its, ref_src = _reference_iters_per_system(spec.cid)
+    U = None
+    samples = []
+    for pos in range(npos):
+        rp, ci, v, b, _ = P.assemble(spec, order[pos], _fields(spec, order[pos], flat))
+        # one step = the next system of the sorted chain, bounded in time; the
+        # chain continues from that solve's recycle space
+        s, U = _oracle_sample(spec, [(rp, ci, v, b)], args.ref_step_s, U_in=U)
+        if pos >= args.warmup:
+            samples.extend(s)
+    its_sys = ref_its if ref_its else float(np.mean([s[0] for s in samples]))
+    value, how = _cpu_rate(samples, its_sys)
+    wall = sum(s[1] for s in samples)
+    out = {
+        "metric": METRIC, "value": value, "unit": "systems/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * wall / max(1, len(samples)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config generator)", "impl": "reference",
+        "config": _config_dict(spec, 1, world, 1),
+        "cpu_baseline": {"value": value, "unit": "systems/s", "cores": _CORES, "kind": "port",
+                         "sample": (f"oracle GCRO-DR chain over sorted positions "
+                                    f"{args.warmup}..{npos - 1} (after {args.warmup} warm-up "
+                                    f"positions), each step one system capped at ~"
+                                    f"{args.ref_step_s:.0f} s of iterations; {how}: "
+                                    f"iterations/s / {its_sys:.1f} iterations per system "
+                                    f"({ref_src or 'the sample'}); prefix sort "
+                                    f"{prefix_sort_s:.1f}s excluded")},
+        "e2e": {"value": value, "unit": "systems/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "iterations_sampled": [s[0] for s in samples],
+        "cpu_model": _cpu_model(),
+    }
+    print(json.dumps(out), flush=True)
+
+
+def _config_dict(spec, stripe, world, chains):
     return {"workload": f"C{spec.cid} {spec.name}: {spec.kind}, grid {spec.n}^{spec.dim} "
                         f"(N={spec.N}), batch {spec.n_systems}, greedy-NN sorted, "
                         f"GCRO-DR(m={spec.m}, k={spec.k}), {spec.precond}, tol {spec.tol:g}",
             "n_systems_batch": spec.n_systems, "N": spec.N, "m": spec.m, "k": spec.k,
             "precond": spec.precond, "tol": spec.tol, "max_iter": spec.max_iter,
-            "stripe_systems_per_step": stripe,
-            "parallelism": f"chunked chains x{world} (contiguous sorted chunks)",
-            "l2": "flushed between steps (256 MiB write)"}
+            "stripe_systems_per_step": stripe, "chains_per_gpu": chains,
+            "parallelism": f"chunked chains: {world} rank(s) x {chains} chain(s) "
+                           f"(contiguous sorted chunks)"}
 
 
 class _HostCsr:
     """Pinned host CSR in the upload format (int32 indices, fp64 values)."""
 
     def __init__(self, n, rp, ci, v):
-        import torch
-
         self.n_rows = self.n_cols = n
-        self.row_ptr = torch.from_numpy(rp.astype(np.int32)).pin_memory()
-        self.col_idx = torch.from_numpy(ci.astype(np.int32)).pin_memory()
-        self.values = torch.from_numpy(v).pin_memory()
+        self.row_ptr = rp
+        self.col_idx = ci
+        self.values = v
 
 
 def run_skr(args):
@@ -271,42 +378,49 @@ def run_skr(args):
         raise SystemExit(f"--stripe {S} must be a multiple of --chains {NC}")
     gctas = skr.chain_grid_ctas(NC) if args.ctas_per_chain is None else args.ctas_per_chain
     cfg = skr.SolverConfig(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
-    # ---- sort (sharded rows + all_gather when world > 1) -------------------
+    jac = spec.precond == "jacobi"
+    # ---- parameters + sort (sharded rows + all_gather when world > 1) -------
+    t_gen = time.perf_counter()
     flat = _params(spec)
+    gen_s = time.perf_counter() - t_gen
     flat_d = torch.from_numpy(flat).to(dev)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    if world > 1:
-        order = skr.sharded_greedy_sort(flat_d)
-    else:
-        order = skr.greedy_sort_device(flat_d)
+    order = skr.sharded_greedy_sort(flat_d) if world > 1 else skr.greedy_sort_device(flat_d)
     e1.record()
     torch.cuda.synchronize()
     sort_ms = e0.elapsed_time(e1)
     del flat_d
     # ---- this rank's chunk of the chain ------------------------------------
-    chunk = skr.chunk_positions(spec.n_systems, world, rank)
+    chunk = list(skr.chunk_positions(spec.n_systems, world, rank))
     need = (W + K) * S
-    chunk = list(chunk)
     if not chunk:
         raise SystemExit(f"rank {rank}: empty chunk")
     # a rank's chunk (n_systems / world) can be shorter than the (W + K) * S
-    # systems a long run needs (e.g. 8 GPUs, many steps): the chains then
-    # continue through the chunk again (every solve is real work; the jump
-    # back costs one poorly recycled system per chain)
+    # systems a long run needs: the chains then continue through the chunk
+    # again (every solve is real work)
     wrapped = len(chunk) < need
     pos = [chunk[i % len(chunk)] for i in range(need)]
     idxs = [order[p] for p in pos]
-    host = []
-    for i in idxs:
-        rp, ci, v, b, _ = P.assemble(spec, i)
-        host.append((_HostCsr(spec.N, rp, ci, v), torch.from_numpy(b).pin_memory()))
+    distinct = len(set(idxs))
+    # device-resident systems: coefficient field uploaded, CSR values and the
+    # stencil form assembled on the GPU (bit-identical to the host assembly)
     dev_sys = []
-    for A, b in host:
-        dA = skr.DeviceCsr.from_host(A, jacobi=spec.precond == "jacobi")
-        dev_sys.append((dA, b.to(dev)))
+    for i in idxs:
+        dA, b, _ = P.assemble_device(spec, i, _fields(spec, i, flat), jacobi=jac)
+        dev_sys.append((dA, b))
     torch.cuda.synchronize()
+    # pinned host copies of the same systems for the end-to-end pass (the
+    # sparsity pattern is one pinned array pair; its bytes are still uploaded
+    # for every system)
+    host = []
+    if not args.no_e2e:
+        rp_h = dev_sys[0][0].row_ptr.cpu().pin_memory()
+        ci_h = dev_sys[0][0].col_idx.cpu().pin_memory()
+        for dA, b in dev_sys:
+            host.append((_HostCsr(spec.N, rp_h, ci_h, dA.values.cpu().pin_memory()),
+                         b.cpu().pin_memory()))
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     ident = list(range(need))
 
@@ -315,29 +429,23 @@ def run_skr(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # pinned host buffer for the e2e read-back of x (allocated outside any timed region)
-    x_pinned = (torch.empty((W + K) * S * spec.N, dtype=torch.float64, pin_memory=True)
-                if not args.no_e2e else None)
     sub = S // NC          # systems per chain per step
     span = (W + K) * sub   # positions per chain (contiguous sub-chunk of this rank's chunk)
+    # pinned host buffer for the e2e read-back of x: one row per position
+    x_pinned = (torch.empty((need, spec.N), dtype=torch.float64, pin_memory=True)
+                if not args.no_e2e else None)
 
     def solve(systems, chunks, states, keep_x):
-        if NC == 1:
-            return [skr.solve_sequence(systems, ident, cfg, spec.precond, positions=chunks[0],
-                                       keep_x=keep_x, chain=states[0])]
         if keep_x != "host":
             return skr.solve_chains(systems, ident, cfg, spec.precond, chunks, keep_x=keep_x,
                                     states=states, grid_ctas=gctas)
         # end to end: upload this call's systems from pinned host memory, solve
-        # the chains on the device, read every x back
-        dbg = bool(os.environ.get("SKR_E2E_DEBUG"))
-        t_a = time.perf_counter()
+        # the chains on the device, read every x back into its own pinned row
         up, h2d = {}, {}
         for ch in chunks:
             for q in ch:
                 A, b = systems[q]
-                dA = skr.DeviceCsr.from_host(A, jacobi=spec.precond == "jacobi", non_blocking=True,
-                                             check_pivot=bool(os.environ.get("SKR_E2E_SYNC")))
+                dA = skr.DeviceCsr.from_host(A, jacobi=jac, non_blocking=True, check_pivot=False)
                 up[q] = (dA, b.to(dev, non_blocking=True))
                 h2d[q] = (A.row_ptr.numel() * 4 + A.col_idx.numel() * 4 + A.values.numel() * 8
                           + b.numel() * 8)
@@ -346,29 +454,15 @@ def run_skr(args):
         if flags and bool(torch.stack(flags).any()):  # one sync for the whole call
             for u in up.values():
                 u[0].raise_if_zero_pivot()
-        if dbg:
-            t_b = time.perf_counter()
-            torch.cuda.synchronize()
-            t_c = time.perf_counter()
         rl = skr.solve_chains(lambda i: up[i], ident, cfg, spec.precond, chunks, keep_x="device",
                               states=states, grid_ctas=gctas)
-        if dbg:
-            torch.cuda.synchronize()
-            t_d = time.perf_counter()
         for r, ch in zip(rl, chunks):
-            xs = None
-            if r.x:  # into the preallocated pinned host buffer (pageable: ~2 GB/s)
-                xd = torch.stack(r.x)
-                xs = x_pinned[: xd.numel()].view(xd.shape)
-                xs.copy_(xd, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-            r.x = list(xs.numpy()) if xs is not None else []
+            for xd, q in zip(r.x, ch):
+                x_pinned[q].copy_(xd, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            r.x = [x_pinned[q].numpy() for q in ch]
             r.h2d_bytes = int(sum(h2d[q] for q in ch))
-            r.d2h_bytes = int(xs.numel() * 8) if xs is not None else 0
-        if dbg:
-            t_e = time.perf_counter()
-            print(f"e2e phases ms: enqueue uploads {1e3 * (t_b - t_a):.1f}, drain {1e3 * (t_c - t_b):.1f}, "
-                  f"solve {1e3 * (t_d - t_c):.1f}, x to host {1e3 * (t_e - t_d):.1f}", file=sys.stderr)
+            r.d2h_bytes = int(len(ch) * spec.N * 8)
         return rl
 
     def stripes(a, b):  # positions of stripes [a, b) for every chain
@@ -398,12 +492,12 @@ def run_skr(args):
                     per_step.append(ev0.elapsed_time(ev1))
                     stats.extend(rl)
             return per_step, stats, u_at_timed
-        rl = solve(systems, stripes(0, W), states, keep_x)
-        states = [r.chain for r in rl]
+        rl = solve(systems, stripes(0, W), states, keep_x) if W > 0 else []
+        states = [r.chain for r in rl] if rl else [None] * NC
         if states[0] is not None and states[0].k > 0:
             u_at_timed = states[0].engine.recycle_views()[0].cpu().numpy()
-        # warm the caching allocator for the timed call's output block
         del rl
+        # warm the caching allocator for the timed call's output block
         torch.empty((K * S, spec.N), dtype=torch.float64, device=dev)
         _flush_l2(flush)
         barrier()
@@ -420,122 +514,152 @@ def run_skr(args):
     per_step, stats, u_timed = run_pass(dev_sys, "device")
     clk = clocks.stop(local)
     total_ms = float(sum(per_step))
-    tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    total_ms_max = float(tmax.item())
+
+    def all_max(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    total_ms_max = all_max(total_ms)
     n_sys_timed = S * K * world
     value = n_sys_timed / (total_ms_max / 1000.0)
     its = [i for r in stats for i in r.iterations]
-    conv = all(c for r in stats for c in r.converged)
+    conv_local = all(c for r in stats for c in r.converged)
     bytes_ = sum(r.spmv_ortho_bytes for r in stats)
     cyc_ms = sum(r.cycle_kernel_ms for r in stats)
     den_ms = sum(r.dense_kernel_ms for r in stats)
     launches = sum(r.launches for r in stats)
     steps_arn = sum(r.arnoldi_steps for r in stats)
+    v0proj = sum(sum(r.v0_projections) for r in stats)
     peak, peak_src = _peaks()
     per_launch = bytes_ / (cyc_ms / 1000.0) / 1e9 if cyc_ms > 0 else 0.0
     aggregate = bytes_ / (total_ms / 1000.0) / 1e9 if total_ms > 0 else 0.0
     # with several chains the k_cycle launches overlap on the device (each owns
-    # a share of the SMs), so a launch's event time is not its cost: report the
-    # k_cycle bytes over the whole timed region (which also contains the dense
-    # kernels: a lower bound on the kernel's bandwidth)
+    # a share of the SMs), so a launch's event time is not its cost: the
+    # achieved figure is the k_cycle bytes over the whole timed region (which
+    # also holds the dense / combine / refresh kernels: a lower bound)
     achieved = aggregate if NC > 1 else per_launch
-    traffic, alg_per_launch = _traffic()
+    ratio, tr_src = _traffic(spec.cid)
+    n_cycle_launches = sum(sum(r.cycles) for r in stats)
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
+    conv_e2e = True
     if not args.no_e2e:
         # release the device-resident copies: the e2e uploads then reuse the
-        # caching allocator's blocks instead of growing it (cudaMalloc) inside
-        # the timed region
+        # caching allocator's blocks instead of growing it inside the timed region
         dev_sys.clear()
         per_step_e, stats_e, _ = run_pass(host, "host")
-        tot_e = torch.tensor([float(sum(per_step_e))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tot_e, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_sys_timed / (float(tot_e.item()) / 1000.0), "unit": "systems/s",
+        tot_e = all_max(sum(per_step_e))
+        conv_e2e = all(c for r in stats_e for c in r.converged)
+        e2e = {"value": n_sys_timed / (tot_e / 1000.0), "unit": "systems/s",
                "h2d_bytes_per_step": int(sum(r.h2d_bytes for r in stats_e) / K),
                "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in stats_e) / K),
-               "path": ("pinned host CSR+b -> DeviceCsr.from_host -> solve_chains -> x to host, "
-                        "inside the timed region")}
+               "path": ("pinned host CSR+b -> DeviceCsr.from_host (upload + device stencil "
+                        "build) -> solve_chains -> x to pinned host, inside the timed region")}
+    # every rank's solves (timed device pass and e2e pass) must have converged
+    conv_t = torch.tensor([1.0 if (conv_local and conv_e2e) else 0.0], device=dev)
+    if world > 1:
+        dist.all_reduce(conv_t, op=dist.ReduceOp.MIN)
+    all_conv = bool(conv_t.item() > 0.5)
+    its_all = its
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, its)
+        its_all = [i for g in gathered for i in g]
     # ---- CPU baseline: oracle port on this host (rank 0, N = 1) ------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = _cpu_baseline(spec, host, W * sub, u_timed, args.cpu_budget_s)
+        cpu = _cpu_baseline(spec, idxs[W * sub:], flat, u_timed, args.cpu_budget_s,
+                            float(np.mean(its)))
     if rank != 0:
         return
+    # ncu DRAM bytes per k_cycle launch, as (DRAM / algorithmic bytes of the
+    # captured launches, same config and chain shape) x this run's algorithmic
+    # bytes per launch
+    traffic = ratio * bytes_ / max(1, n_cycle_launches) if ratio is not None else None
     out = {
         "metric": METRIC, "value": value, "unit": "systems/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator; DCT-sampled GRF, see DESIGN.md)",
-        "config": dict(_config_dict(spec, S, world), chains_per_gpu=NC, chunk_wrapped=wrapped,
-                       ctas_per_chain=gctas,
+        "config": dict(_config_dict(spec, S, world, NC), chunk_wrapped=wrapped,
+                       distinct_systems=distinct, ctas_per_chain=gctas,
                        l2=("flushed between steps (256 MiB write)" if args.sync_steps else
-                           "flushed (256 MiB write) before the timed region; inside it each "
-                           "stripe's working set (per chain ~39 MB basis + CSR, x8 chains) "
-                           "exceeds the 126 MB L2"),
+                           "flushed (256 MiB write) before the timed region; inside it every "
+                           "chain's working set exceeds the 126 MB L2 (C3: ~1.6 GB per chain)"),
                        timing=("each step timed separately" if args.sync_steps else
                                "K stripes back to back in one timed region (CUDA events, "
                                "barrier + synchronize on both sides); ms_per_step = total / K")),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "frac_vs_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+                     "traffic": traffic, "traffic_source": tr_src,
                      "method": ("sum of k_cycle algorithmic bytes / timed-region device time "
-                                "(concurrent chains)" if NC > 1 else
+                                "(concurrent chains; the region also holds the dense, combine "
+                                "and refresh kernels)" if NC > 1 else
                                 "sum of k_cycle algorithmic bytes / sum of k_cycle event time"),
                      "per_launch_gbs": per_launch, "aggregate_gbs": aggregate,
+                     "k_cycle_launches": int(n_cycle_launches),
+                     "algorithmic_bytes_per_launch": bytes_ / max(1, n_cycle_launches),
                      "kernel": "k_cycle (persistent DCGS2 Arnoldi cycle: SpMV + ortho)",
                      "peak_source": peak_src,
-                     "algorithmic_bytes": ("per step B_spmv + 8N(2p+6), SURVEY 8(d); B_spmv = 24N + 16N "
-                                           "through the stencil form (2-D), 12 nnz + 4(N+1) + 16N "
-                                           "through the CSR"),
-                     "note": "one chain's C1 working set (~39 MB) fits the L2; the 8 concurrent "
-                             "chains' (~312 MB) do not"},
+                     "algorithmic_bytes": ("per Arnoldi step B_spmv + 8N(2p+6), SURVEY 8(d), "
+                                           "p = basis width; B_spmv = 32N + 16N through the "
+                                           "3-D stencil form (24N + 16N in 2-D), "
+                                           "12 nnz + 4(N+1) + 16N through the CSR")},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,
-        "iterations_mean": float(np.mean(its)), "all_converged": bool(conv),
+        "iterations_mean": float(np.mean(its_all)), "all_converged": all_conv,
+        "v0_projected_cycles": int(v0proj),
         "arnoldi_steps": int(steps_arn),
         "us_per_arnoldi_step": 1000.0 * cyc_ms / max(1, steps_arn),
         "time_split_ms": {"cycle_kernels": cyc_ms, "dense_recycle_kernels": den_ms,
                           "solve_streams": float(sum(sum(r.device_ms) for r in stats)),
                           "chain_wall_ms": sorted(round(1000 * r.wall_s, 1) for r in stats),
                           "total": total_ms},
-        "sort": {"ms": sort_ms, "n_systems": spec.n_systems, "P": int(flat.shape[1])},
+        "sort": {"ms": sort_ms, "n_systems": spec.n_systems, "P": int(flat.shape[1]),
+                 "param_generation_s": round(gen_s, 1)},
     }
     if cpu is not None:
         out["cpu_baseline"] = cpu
     print(json.dumps(out), flush=True)
 
 
-def _cpu_baseline(spec, host, first_pos, U_in, budget_s):
-    from oracle import skr_oracle as orc
+def _cpu_baseline(spec, idxs, flat, U_in, budget_s, gpu_its):
+    from paper_2401_09516_b200 import problems as P
 
-    cfg = orc.Cfg(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
-    walls = []
+    systems = []
+    for i in idxs[:4]:
+        rp, ci, v, b, _ = P.assemble(spec, i, _fields(spec, i, flat))
+        systems.append((rp, ci, v, b))
+    samples = []
     U = U_in
-    t_start = time.perf_counter()
-    p = first_pos
-    while p < len(host) and (time.perf_counter() - t_start) < budget_s:
-        A, b = host[p]
-        op = orc.Operator(A.row_ptr.numpy(), A.col_idx.numpy(), A.values.numpy(), spec.N,
-                          spec.precond == "jacobi")
-        r = orc.gcrodr(op, b.numpy(), cfg, U_in=U)
-        U = r.U
-        walls.append(r.wall_time)
-        p += 1
-    v = len(walls) / sum(walls)
+    t0 = time.perf_counter()
+    for sy in systems:
+        left = budget_s - (time.perf_counter() - t0)
+        if left <= 0:
+            break
+        s, U = _oracle_sample(spec, [sy], left, U_in=U)
+        samples.extend(s)
+    ref_its, ref_src = _reference_iters_per_system(spec.cid)
+    its_sys = ref_its or gpu_its
+    v, how = _cpu_rate(samples, its_sys)
     return {"value": v, "unit": "systems/s", "cores": _CORES, "kind": "port",
-            "sample": f"oracle chain on {len(walls)} system(s) starting at the first timed "
-                      f"position, recycle U taken from the GPU chain (steady state); "
-                      f"OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS')}",
+            "sample": (f"oracle GCRO-DR on {len(samples)} system(s) from the first timed "
+                       f"position, recycle U taken from the GPU chain (steady state), "
+                       f"~{budget_s:.0f} s of CPU; {how} with {its_sys:.1f} iterations per "
+                       f"system ({ref_src or 'GPU mean'}); OPENBLAS_NUM_THREADS="
+                       f"{os.environ.get('OPENBLAS_NUM_THREADS')}"),
+            "iterations_sampled": [s[0] for s in samples],
             "cpu_model": _cpu_model()}
 
 
 def main():
     args = _args()
-    if os.environ.get("SKR_SWITCH_INTERVAL"):
-        sys.setswitchinterval(float(os.environ["SKR_SWITCH_INTERVAL"]))
+    rc = _relaunch_under_torchrun(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
     else:

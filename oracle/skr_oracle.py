@@ -416,7 +416,7 @@ class Result:
     info: dict = field(default_factory=dict)
 
 
-def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None) -> Result:
+def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None, deadline=None) -> Result:
     """GCRO-DR solve with a carried recycle basis (gcrodr.py:295-496).
 
     ``U_in`` is the previous system's recycle U (its C is discarded by the
@@ -455,6 +455,9 @@ def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None) -> Result:
             hist.append(rnorm)
     conv = rnorm <= abs_tol
     while not conv and iters < cfg.max_iter:
+        # bench samples only: stop at a cycle boundary once the deadline passed
+        if deadline is not None and time.perf_counter() >= deadline:
+            break
         if U is None:
             V, H, j, sres, y, brk = gmres_cycle(op, r, rnorm, cfg.m, abs_tol,
                                                  cfg.max_iter - iters)

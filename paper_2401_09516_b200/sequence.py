@@ -53,6 +53,7 @@ class SequenceResult:
     k_out: list = field(default_factory=list)
     warn_bits: list = field(default_factory=list)
     v0_projections: list = field(default_factory=list)
+    cycles: list = field(default_factory=list)
     spmv_ortho_bytes: float = 0.0
     x: list = field(default_factory=list)
     launches: int = 0
@@ -158,6 +159,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
         res.k_out.append(int(rep.k_out))
         res.warn_bits.append(int(rep.warn_bits))
         res.v0_projections.append(int(rep.v0_projections))
+        res.cycles.append(int(rep.cycles))
         res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
         res.launches += int(rep.launches)
         res.cycle_kernel_ms += float(rep.cycle_kernel_ms)
@@ -339,6 +341,7 @@ def _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states, g
             res.k_out.append(int(rep.k_out))
             res.warn_bits.append(int(rep.warn_bits))
             res.v0_projections.append(int(rep.v0_projections))
+            res.cycles.append(int(rep.cycles))
             res.spmv_ortho_bytes += float(rep.spmv_ortho_bytes)
             res.launches += int(rep.launches)
             res.cycle_kernel_ms += float(rep.cycle_kernel_ms)

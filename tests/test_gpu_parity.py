@@ -309,7 +309,15 @@ def test_chain_small_golden(name):
         assert res.converged[pos]
         err = np.linalg.norm(res.x[pos] - g["x"][pos]) / np.linalg.norm(g["x"][pos])
         assert err < 1e-6, (pos, err)
-        assert res.true_rel[pos] <= 10 * 1e-8 * max(1.0, 1.0) or jac
+        # the reference's criterion ||M^-1 (b - A x)|| <= tol ||M^-1 b||,
+        # re-checked on the host (gcrodr.py:348-349, :442) ...
+        A, b = systems[order[pos]]
+        S = A.to_scipy()
+        d = S.diagonal() if jac else np.ones(A.n_rows)
+        rel = np.linalg.norm((b - S @ res.x[pos]) / d) / np.linalg.norm(b / d)
+        assert rel <= 1.05e-8, (pos, rel)
+        # ... and the unpreconditioned one agrees with the reference's report
+        assert res.true_rel[pos] <= 1.5 * g["true_rel"][pos] + 1e-12, (pos, res.true_rel[pos])
     dev = np.abs(it_gpu - it_ref) / it_ref
     print(name, "gpu", list(it_gpu), "ref", list(it_ref))
     assert dev.mean() <= 0.05, f"chain-mean iteration deviation {dev.mean():.3f}"
@@ -350,7 +358,9 @@ def test_first_system_matches_oracle_exactly():
     assert rep.converged and ref.converged
     assert abs(rep.iterations - ref.iterations) <= 0.05 * ref.iterations
     assert np.linalg.norm(rep.x - ref.x) / np.linalg.norm(ref.x) < 1e-6
-    assert len(rep.residual_history) == len(ref.history) or True
+    # one history entry per iteration (plus the initial norm): the lengths
+    # differ exactly by the iteration difference
+    assert len(rep.residual_history) - len(ref.history) == rep.iterations - ref.iterations
     np.testing.assert_allclose(rep.residual_history[:5], ref.history[:5], rtol=1e-9)
     assert out.k == ref.U.shape[1]
 
@@ -552,3 +562,36 @@ def test_stencil_rectangular_grids_and_solve():
         d = S.diagonal()
         assert rep.converged
         assert np.linalg.norm((b - S @ rep.x) / d) <= 1.05e-10 * np.linalg.norm(b / d)
+
+
+def test_c3_eight_chain_shape_converges():
+    """Regression for the C3 DCGS2 breakdown (round-1 VERDICT): 16 C3 systems
+    (N = 2,097,152, GCRO-DR(40, 20), Jacobi) as 8 concurrent chains of 2 on
+    one GPU (64 CTAs each, the bench shape). In this shape the reference's
+    V_0 = r / beta let |C^T r| grow x2-4 per cycle on some systems until the
+    Pythagorean norm reported a spurious breakdown (system 5 stopped at
+    4e-5). Every system must meet the reference criterion
+    ||M^-1 (b - A x)|| <= tol ||M^-1 b||, re-checked here with cuSPARSE (torch)."""
+    skr = _skr()
+    from paper_2401_09516_b200 import problems as P
+
+    spec = _spec(3)
+    cfg = skr.SolverConfig(m=spec.m, k=spec.k, tol=spec.tol, max_iter=spec.max_iter)
+    ns, nch = 16, 8
+    systems = [P.assemble_device(spec, i)[:2] for i in range(ns)]
+    torch.cuda.synchronize()
+    chunks = skr.split_chunks(list(range(ns)), nch)
+    res = skr.solve_chains(systems, list(range(ns)), cfg, spec.precond, chunks, keep_x="device",
+                           grid_ctas=skr.chain_grid_ctas(nch))
+    for ch, r in zip(chunks, res):
+        for q, i in enumerate(ch):
+            dA, b = systems[i]
+            assert r.converged[q], (i, r.iterations[q], r.true_rel[q])
+            S = torch.sparse_csr_tensor(dA.row_ptr.long(), dA.col_idx.long(), dA.values,
+                                        size=(dA.n, dA.n))
+            x = r.x[q]
+            d = dA.diag
+            res_v = (b - (S @ x.unsqueeze(1)).squeeze(1)) / d
+            rel = float(torch.linalg.norm(res_v) / torch.linalg.norm(b / d))
+            assert rel <= 1.05 * spec.tol, (i, rel)
+            assert 300 <= r.iterations[q] <= 900, (i, r.iterations[q])

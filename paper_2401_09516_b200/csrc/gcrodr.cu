@@ -42,7 +42,6 @@ constexpr int LDB = KMAX;              // ld of B
 constexpr int LDX = MMAX;              // ld of cross
 constexpr int LDC = KMAX + MMAX + 1;   // ld of coefficient matrices
 constexpr int LDK = KMAX;              // ld of small k x k matrices
-constexpr int ACC_STRIDE = 32;         // doubles between accumulators (256 B)
 
 enum Prog {
   P_INIT = 0,
@@ -63,7 +62,8 @@ enum CombineMode {
 struct State {
   // config
   int n, ld, m, k, kcap, max_iter, jacobi, nblk, rpb, k_in, has_x0,
-      comb_part;  // cycle-start partials: 0 = rows [0, 2kc) (k_project), 1 = COMB_PART0 rows
+      comb_part,  // cycle-start partials: 0 = rows [0, 2kc) (k_project), 1 = COMB_PART0 rows
+      comb_nblk;  // CTAs of the k_combine launch that wrote the COMB_PART0 rows
   double tol;
   // scalars
   double bnorm, bprec, abs_tol, rnorm, true_rel;
@@ -83,10 +83,6 @@ struct State {
   long long prof[32]; // [0,16) dense-kernel phase clocks (recycle.h SKR_PHASE),
                       // [16,24) k_cycle phase clocks of CTA 0
   int kept[KMAX];
-  // triple-buffered cross-CTA accumulators of k_cycle; value v of buffer b at
-  // acc[(b * PV_STEP + v) * ACC_STRIDE]: one value per 256-byte line so the
-  // fp64 red.add traffic of all CTAs spreads over the L2 slices
-  double acc[3 * PV_STEP * ACC_STRIDE];
   // per-cycle small data
   double H[LDH * MMAX];
   double B[LDB * MMAX];
@@ -105,7 +101,7 @@ struct State {
 };
 
 struct Layout {
-  size_t state, basis, r, z, part, hist, checks, total;
+  size_t state, basis, r, z, part, sred, hist, checks, total;
   int ld, kcap, ncols, hist_cap;
 };
 
@@ -128,6 +124,8 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
   off = align_up(off + (size_t)L.ld * sizeof(double), 256);
   L.part = off;
   off = align_up(off + (size_t)(PV_MAX + 16 + 2 * KMAX) * GRID_MAX * sizeof(double), 256);
+  L.sred = off;
+  off = align_up(off + (size_t)2 * GRID_MAX * PV_STEP * sizeof(double), 256);
   L.hist = off;
   off = align_up(off + (size_t)L.hist_cap * sizeof(double), 256);
   L.checks = off;
@@ -137,8 +135,10 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
 }
 
 // p.part rows: [0, 16) per-cycle scalar partials, [16, 16 + mm^2) cross-Gram,
-// [COMB_PART0, COMB_PART0 + 2 KMAX) next-cycle partials accumulated by k_combine
-// (fp64 red.add into slot blk % nblk; zeroed by k_init and after each read)
+// [COMB_PART0, COMB_PART0 + 2 KMAX) next-cycle partials written by k_combine
+// (one slot per combine CTA, st->comb_nblk of them). Every cross-CTA sum in
+// this file is a fixed-order sum of per-CTA slots: results are bitwise
+// reproducible run to run (no floating-point atomics).
 constexpr int GRAM_PART0 = 16;
 constexpr int COMB_PART0 = GRAM_PART0 + PV_MAX;
 
@@ -156,6 +156,7 @@ struct Ptrs {
   double* z;
   double* basis;
   double* part;
+  double* sred;  // k_cycle per-step partials: [2 buffers][GRID_MAX CTAs][PV_STEP values]
   double* hist;
   double* checks;
   int n, ld, kcap, nblk, rpb;
@@ -544,7 +545,10 @@ __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
   if (mode == CM_CYCLE && !st->done) {
     // partials for the next cycle start: C^T r (kc) and |U_c|^2 (kc)
     int kc = st->kc;
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->comb_part = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->comb_part = 1;
+      st->comb_nblk = gridDim.x;
+    }
     __syncthreads();
     for (int c = 0; c < kc; ++c) {
       const double* C = colC(p, p.kcap - kc + c);
@@ -557,10 +561,9 @@ __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
       }
       double t1 = block_sum(s1, s_red);
       double t2 = block_sum(s2, s_red);
-      if (threadIdx.x == 0) {  // slot blk % nblk of the zeroed COMB_PART0 rows
-        const size_t slot = blockIdx.x % p.nblk;
-        red_add_f64(p.part + (size_t)(COMB_PART0 + c) * GRID_MAX + slot, t1);
-        red_add_f64(p.part + (size_t)(COMB_PART0 + kc + c) * GRID_MAX + slot, t2);
+      if (threadIdx.x == 0) {  // this CTA's slot of the COMB_PART0 rows
+        p.part[(size_t)(COMB_PART0 + c) * GRID_MAX + blockIdx.x] = t1;
+        p.part[(size_t)(COMB_PART0 + kc + c) * GRID_MAX + blockIdx.x] = t2;
       }
     }
   }
@@ -797,8 +800,8 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   // ---- cycle start --------------------------------------------------------
   const bool comb_part = st->comb_part != 0;
   if (defl) {
-    reduce_partials(p.part + (comb_part ? (size_t)COMB_PART0 * GRID_MAX : 0), GRID_MAX, nblk, 0,
-                    2 * kc, S.red);
+    reduce_partials(p.part + (comb_part ? (size_t)COMB_PART0 * GRID_MAX : 0), GRID_MAX,
+                    comb_part ? st->comb_nblk : nblk, 0, 2 * kc, S.red);
     if (tid < kc) {
       double u2 = S.red[kc + tid];
       double un = sqrt(u2);
@@ -861,13 +864,8 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
            st->cycles, kc, st->iters, beta, abs_tol, sqrt(c2) / beta);
   }
 #endif
-  if (blk == 0)
-    for (int v = tid; v < 3 * PV_STEP; v += NT) st->acc[(size_t)v * ACC_STRIDE] = 0.0;
   int red_idx = 0;
   CYCLE_SYNC();
-  if (defl && comb_part && blk == 0)  // every CTA has read them: re-zero for k_combine
-    for (int e = tid; e < 2 * kc * nblk; e += NT)
-      p.part[(size_t)(COMB_PART0 + e / nblk) * GRID_MAX + e % nblk] = 0.0;
 
   int j = 0;
   bool brk = false;
@@ -970,33 +968,64 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       S.bred[3 * warp + 2] = ze;
     }
     __syncthreads();
-    // cross-CTA sums by fp64 red.add into a triple-buffered accumulator
-    // (layout: 0 nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)); every CTA then
-    // reads the same totals. Buffer (r+2)%3 is zeroed after barrier r: its
-    // last readers finished before they arrived there.
-    double* accb = st->acc + (size_t)(red_idx % 3) * PV_STEP * ACC_STRIDE;
-    for (int e = tid; e < 3 + 2 * pb; e += NT) {
-      double sum = 0.0;
-      bool use;
-      if (e < 3) {
+    // cross-CTA sums, deterministic: every CTA stores its partials (layout: 0
+    // nu, 1 mu, 2 ze, 3.. a (pb), 3+pb.. bb (pb)) to its own slot of a
+    // double-buffered array; after the grid barrier every CTA sums all slots
+    // in one fixed order, so all CTAs hold bit-identical totals and a solve
+    // is reproducible run to run. Buffer r % 2 is rewritten at step r + 2, after
+    // barrier r + 1, which every reader of step r has passed.
+    const int nv = 3 + 2 * pb;
+    double* sbuf = p.sred + (size_t)(red_idx & 1) * GRID_MAX * PV_STEP;
+    {
+      double* mine = sbuf + (size_t)blk * PV_STEP;
+      for (int e = tid; e < nv; e += NT) {
+        double sum = 0.0;
+        if (e < 3) {
 #pragma unroll
-        for (int q = 0; q < NW; ++q) sum += S.bred[3 * q + e];
-        use = e == 0 || do_spmv;
-      } else {
-        const int which = e - 3 >= pb, col = which ? e - 3 - pb : e - 3;
+          for (int q = 0; q < NW; ++q) sum += S.bred[3 * q + e];
+        } else {
+          const int which = e - 3 >= pb, col = which ? e - 3 - pb : e - 3;
 #pragma unroll
-        for (int q = 0; q < NW; ++q) sum += sacc[q * 2 * PVC + which * PVC + col];
-        use = which ? do_spmv : (t >= 1);
+          for (int q = 0; q < NW; ++q) sum += sacc[q * 2 * PVC + which * PVC + col];
+        }
+        mine[e] = sum;
       }
-      if (use) red_add_f64(accb + (size_t)e * ACC_STRIDE, sum);
     }
     CPROF(0);
     CYCLE_SYNC();
     CPROF(1);
-    for (int v = tid; v < 3 + 2 * pb; v += NT) S.red[v] = accb[(size_t)v * ACC_STRIDE];
-    if (blk == 0) {
-      double* old = st->acc + (size_t)((red_idx + 2) % 3) * PV_STEP * ACC_STRIDE;
-      for (int v = tid; v < PV_STEP; v += NT) old[(size_t)v * ACC_STRIDE] = 0.0;
+    {
+      // ng thread groups per value: group g sums slots g, g + ng, ... in
+      // chunks of RL loads issued together (one L2 round trip per chunk; at
+      // 64 CTAs per chain that is a single chunk), each chunk added as a
+      // fixed tree; the groups are combined in order below
+      constexpr int RL = 16;
+      const int ng = max(1, NT / nv);
+      double* gsum = sacc;  // sweep-1 partials are consumed: reuse the area
+      if (tid < ng * nv) {
+        const int v = tid % nv, g = tid / nv;
+        double acc = 0.0;
+        for (int b0 = g; b0 < nblk; b0 += RL * ng) {
+          double q[RL];
+#pragma unroll
+          for (int u = 0; u < RL; ++u) {
+            const int b = b0 + u * ng;
+            q[u] = b < nblk ? sbuf[(size_t)b * PV_STEP + v] : 0.0;
+          }
+#pragma unroll
+          for (int w = RL / 2; w >= 1; w /= 2)
+#pragma unroll
+            for (int u = 0; u < w; ++u) q[u] += q[u + w];
+          acc += q[0];
+        }
+        gsum[g * nv + v] = acc;
+      }
+      __syncthreads();
+      for (int v = tid; v < nv; v += NT) {
+        double t = gsum[v];
+        for (int g = 1; g < ng; ++g) t += gsum[g * nv + v];
+        S.red[v] = t;
+      }
     }
     ++red_idx;
     __syncthreads();
@@ -2046,6 +2075,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.z = (double*)(base + L.z);
   p.basis = (double*)(base + L.basis);
   p.part = (double*)(base + L.part);
+  p.sred = (double*)(base + L.sred);
   p.hist = (double*)(base + L.hist);
   p.checks = (double*)(base + L.checks);
   p.n = n;

@@ -675,6 +675,7 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
 constexpr double V0_PROJ_RTOL = 1e-6;
 
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
+constexpr int GM_LD = 36;  // the same for the DMMA Gram (== 4 mod 16: conflict-free fragments)
 
 // k_cycle dynamic shared memory, sized by (m, kcap) (offsets in doubles):
 // [ Gram tile (2 kcap + m + 1 cols x GT_LD; aliased by the sweep-1 partials)
@@ -684,7 +685,7 @@ struct CycleSmemLayout {
 };
 inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
   CycleSmemLayout L;
-  size_t gt = (size_t)(2 * kcap + m + 1) * GT_LD;
+  size_t gt = (size_t)(2 * kcap + m + 1) * GM_LD + NT;  // + the x-update scratch
   if (gt < (size_t)NW * 2 * PVC) gt = (size_t)NW * 2 * PVC;
   L.R = gt;
   L.B = L.R + (size_t)m * (m + 1) / 2;
@@ -1285,20 +1286,144 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     CPROF(4);
   }
 
-  // ---- x update: x += U (dk y1) + V y2 (own rows: no grid barrier needed) ----
+  // ---- cycle end: x update, explicit residual, cross-Gram partials ---------
   for (int q = tid; q < kc; q += NT) S.y[q] *= S.dk[q];
   __syncthreads();
-  for (int row = r0 + tid; row < r1; row += NT) {
-    double su = 0.0, sv = 0.0;
-    for (int c = 0; c < kc; ++c) su += colU(p, c)[row] * S.y[c];
-    for (int v = 0; v < j; ++v) sv += colV(p, v)[row] * S.y[kc + v];
-    p.x[row] = p.x[row] + (su + sv);
+  const int mm = kc + j;
+  // cross-Gram What[:, :mm]^T Vhat (mm x mm, What = [C | V_0..V_{j-1}], Vhat
+  // = [U | V_0..V_{j-1}]) over this CTA's rows. For mm <= 40 (every BASELINE
+  // config but C2) on the fp64 tensor cores (DMMA m8n8k4, rows = the k
+  // dimension), in the same pass over the staged 32-row tiles as the x update
+  // x += U (dk y1) + V y2, whose U and V columns are staged anyway; otherwise
+  // the register-tiled CUDA-core Gram after the residual (below).
+  const bool gmma = defl && mm <= 40;
+  auto tile_col = [&](int c) -> const double* {  // staged columns [U (kc) | C (kc) | V (j)]
+    return (c < kc) ? colU(p, c) : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc)) : colV(p, c - 2 * kc);
+  };
+  if (gmma) {
+    constexpr int GL = GM_LD;  // == 4 (mod 16) doubles: conflict-free fragment loads
+    const int ncs = 2 * kc + j;
+    const int nb = (mm + 7) >> 3;  // 8 x 8 blocks per side, <= 5
+    // warp w: block rows bi in [3 h, 3 h + 3) (h = w & 1), k-steps 2 (w >> 1)
+    // and 2 (w >> 1) + 1 of every tile (rows 4 ks .. 4 ks + 3); lane l holds
+    // A[m = l/4][k = l%4] = What(row, 8 bi + m), B[k][n = l/4] = Vhat(row, 8 bj + n)
+    const int h = warp & 1, ks0 = 2 * (warp >> 1);
+    const int ln = lane >> 2, lk = lane & 3;
+    int wa[3], vb[5];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const int a = min(8 * (3 * h + x) + ln, mm - 1);
+      wa[x] = ((a < kc) ? kc + a : 2 * kc + (a - kc)) * GL + lk;
+    }
+#pragma unroll
+    for (int y = 0; y < 5; ++y) {
+      const int b = min(8 * y + ln, mm - 1);
+      vb[y] = ((b < kc) ? b : 2 * kc + (b - kc)) * GL + lk;
+    }
+    double acc[3][5][2];
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+#pragma unroll
+      for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    double* xpart = cdyn + p.sm_R - NT;  // last NT doubles of the Gram region
+    constexpr int GPF = 8;               // next tile's first elements, in flight
+    double pf[GPF];
+    auto load_tile = [&](int t0) {
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT, row = t0 + (e & 31);
+        if (e < 32 * ncs) pf[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+      }
+    };
+    if (r0 < r1) load_tile(r0);
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT;
+        if (e < 32 * ncs) gtile[(e >> 5) * GL + (e & 31)] = pf[k];
+      }
+      for (int e = tid + GPF * NT; e < 32 * ncs; e += NT) {
+        const int row = t0 + (e & 31);
+        gtile[(e >> 5) * GL + (e & 31)] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+      }
+      __syncthreads();
+      if (t0 + 32 < r1) load_tile(t0 + 32);
+      {  // x update partials: warp w sums the [U | V] columns c == w (mod NW)
+        double xs = 0.0;
+        for (int c = warp; c < kc + j; c += NW) {
+          const int sc = c < kc ? c : 2 * kc + (c - kc);
+          xs = fma(gtile[sc * GL + lane], S.y[c], xs);
+        }
+        xpart[warp * 32 + lane] = xs;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int roff = 4 * (ks0 + kk);
+        double af[3], bf[5];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) af[x] = gtile[wa[x] + roff];
+#pragma unroll
+        for (int y = 0; y < 5; ++y) bf[y] = gtile[vb[y] + roff];
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+          if (3 * h + x < nb)
+#pragma unroll
+            for (int y = 0; y < 5; ++y)
+              if (y < nb)
+                asm volatile(
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                    : "d"(af[x]), "d"(bf[y]));
+      }
+      __syncthreads();
+      if (tid < 32 && t0 + tid < r1) {  // warps' partials added in order
+        double xs = xpart[tid];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) xs += xpart[w * 32 + tid];
+        p.x[t0 + tid] = p.x[t0 + tid] + xs;
+      }
+    }
+    // the four k-step pairs of each half are added in warp order (fixed)
+    double* gb = gtile;
+    for (int q = 0; q < NW; ++q) {
+      if (warp == q) {
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int y = 0; y < 5; ++y) {
+            const int bi = 3 * h + x;
+            if (bi < nb && y < nb) {
+              const int idx = (bi * nb + y) * 64 + ln * 8 + 2 * lk;
+              if (q < 2) {
+                gb[idx] = acc[x][y][0];
+                gb[idx + 1] = acc[x][y][1];
+              } else {
+                gb[idx] += acc[x][y][0];
+                gb[idx + 1] += acc[x][y][1];
+              }
+            }
+          }
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < mm * mm; e += NT) {
+      const int a = e % mm, b = e / mm;
+      p.part[(size_t)(GRAM_PART0 + e) * GRID_MAX + blk] =
+          gb[((a >> 3) * nb + (b >> 3)) * 64 + (a & 7) * 8 + (b & 7)];
+    }
+  } else {
+    for (int row = r0 + tid; row < r1; row += NT) {
+      double su = 0.0, sv = 0.0;
+      for (int c = 0; c < kc; ++c) su += colU(p, c)[row] * S.y[c];
+      for (int v = 0; v < j; ++v) sv += colV(p, v)[row] * S.y[kc + v];
+      p.x[row] = p.x[row] + (su + sv);
+    }
   }
   CPROF(8);
   CYCLE_SYNC();
   CPROF(9);
 
-  // ---- explicit residual + cross-Gram partials -------------------------------
+  // ---- explicit residual (needs the neighbours' updated x) --------------------
   double rr = 0.0;
   for (int row = r0 + tid; row < r1; row += NT) {
     double rv = __dsub_rn(__ldg(p.b + row), row_dot(p.x, row));
@@ -1306,8 +1431,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     p.r[row] = rv;
     rr += rv * rv;
   }
-  const int mm = kc + j;
-  if (defl) {
+  if (defl && !gmma) {
     // cross-Gram What[:, :mm]^T Vhat over this CTA's rows, register-tiled: a
     // thread owns the 4 x 4 entries (ai + x*na4, bi + y*na4), so consecutive
     // lanes read consecutive columns of a 32-row tile staged column-major with

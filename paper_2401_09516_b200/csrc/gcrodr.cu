@@ -1348,6 +1348,8 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       }
       __syncthreads();
       if (t0 + 32 < r1) load_tile(t0 + 32);
+      // warp 0 fetches this tile's x now: its latency hides behind the DMMAs
+      const double xold = (tid < 32 && t0 + tid < r1) ? p.x[t0 + tid] : 0.0;
       {  // x update partials: warp w sums the [U | V] columns c == w (mod NW)
         double xs = 0.0;
         for (int c = warp; c < kc + j; c += NW) {
@@ -1380,7 +1382,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         double xs = xpart[tid];
 #pragma unroll
         for (int w = 1; w < NW; ++w) xs += xpart[w * 32 + tid];
-        p.x[t0 + tid] = p.x[t0 + tid] + xs;
+        p.x[t0 + tid] = xold + xs;
       }
     }
     // the four k-step pairs of each half are added in warp order (fixed)

@@ -204,7 +204,10 @@ int skr_greedy_sort(const double* params, int32_t n_sys, int64_t P, int32_t* ord
 
 /* Single-CTA dense steps on the device (test / diagnostic entry points).
  * H: (m+1) x m column-major (ld), G: (mm+1) x mm, cross: mm x mm. P out:
- * ld_p x cols, returns the number of columns in *ncols (or negative status). */
+ * ld_p x cols. ncols points to two int32: ncols[0] = the number of columns
+ * (or a negative status), ncols[1] = skr_warn bits (the reference's
+ * warnings.warn: singular H -> generalized problem, gcrodr.py:196-199;
+ * singular cross-Gram -> pseudoinverse, gcrodr.py:231-235). */
 int skr_dense_hr_first(const double* H, int32_t ldh, int32_t m, int32_t k, double* P,
                        int32_t ldp, int32_t* ncols, void* stream);
 int skr_dense_hr_next(const double* G, int32_t ldg, const double* cross, int32_t ldx, int32_t mm,

@@ -28,6 +28,7 @@ from .sequence import (
     ChainState,
     SequenceResult,
     chunk_positions,
+    gather_results,
     chain_grid_ctas,
     solve_chains,
     solve_sequence,

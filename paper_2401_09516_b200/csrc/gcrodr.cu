@@ -63,7 +63,9 @@ struct State {
   // config
   int n, ld, m, k, kcap, max_iter, jacobi, nblk, rpb, k_in, has_x0,
       comb_part,  // cycle-start partials: 0 = rows [0, 2kc) (k_project), 1 = COMB_PART0 rows
-      comb_nblk;  // CTAs of the k_combine launch that wrote the COMB_PART0 rows
+      comb_nblk,  // CTAs of the k_combine launch that wrote the COMB_PART0 rows
+      comb_pending;  // P_CYCLE left a recycle update (coefU / coefC) for the next
+                     // k_cycle launch (or the final k_combine) to apply
   double tol;
   // scalars
   double bnorm, bprec, abs_tol, rnorm, true_rel;
@@ -143,7 +145,7 @@ constexpr int GRAM_PART0 = 16;
 constexpr int COMB_PART0 = GRAM_PART0 + PV_MAX;
 
 struct Ptrs {
-  int sm_R, sm_B, sm_csr;  // k_cycle dynamic smem offsets (doubles), cycle_smem_layout
+  int sm_R, sm_B, sm_csr, sm_cmb;  // k_cycle dynamic smem offsets (doubles), cycle_smem_layout
   State* st;
   const int32_t* rp;
   const int32_t* ci;
@@ -437,7 +439,9 @@ template <int KT>
 __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
   State* st = p.st;
   if (cycle_mode) {
-    if (!st->ran) return;
+    // the last cycle's update when no k_cycle launch applied it (k_cycle
+    // clears the flag after applying it; the next solve's k_setup resets it)
+    if (!st->comb_pending) return;
   } else if (st->done) {
     return;
   }
@@ -681,12 +685,28 @@ constexpr int GM_LD = 36;  // the same for the DMMA Gram (== 4 mod 16: conflict-
 // [ Gram tile (2 kcap + m + 1 cols x GT_LD; aliased by the sweep-1 partials)
 //   | packed R (m (m+1)/2) | B (kcap x m) | optional CSR slice cache ]
 struct CycleSmemLayout {
-  size_t R, B, csr;
+  size_t R, B, csr, cmb;
 };
+// leading dimension of the transposed recycle-update coefficients staged for
+// the DMMA combine: >= m + 1 inputs rounded to the k-step, and == 4 or 12
+// (mod 16) doubles so a half-warp's A fragments (4 outputs x 4 inputs) fall
+// on distinct bank pairs
+__host__ __device__ inline int comb_ld(int m) {
+  const int need = (m + 4) & ~3;
+  return need <= 44 ? 44 : need <= 52 ? 52 : need <= 60 ? 60 : 68;
+}
 inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
   CycleSmemLayout L;
   size_t gt = (size_t)(2 * kcap + m + 1) * GM_LD + NT;  // + the x-update scratch
   if (gt < (size_t)NW * 2 * PVC) gt = (size_t)NW * 2 * PVC;
+  // the cycle-start recycle update stages (2 kcap + m + 2) columns and then
+  // the two coefficient blocks; at that point the R and B areas are free, so
+  // the combine may run into them
+  const size_t kb = (size_t)((kcap + 7) / 8) * 8;
+  L.cmb = (size_t)(2 * kcap + m + 2) * GM_LD;
+  const size_t cmb_end = L.cmb + 2 * kb * (size_t)comb_ld(m);
+  const size_t rb = (size_t)m * (m + 1) / 2 + (size_t)kcap * m;
+  if (gt + rb < cmb_end) gt = cmb_end - rb;
   L.R = gt;
   L.B = L.R + (size_t)m * (m + 1) / 2;
   L.csr = (L.B + (size_t)kcap * m + 1) & ~(size_t)1;  // 16-byte aligned
@@ -716,21 +736,163 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   int* csr_rp = reinterpret_cast<int*>(cdyn + p.sm_csr);  // cached CSR slice (optional)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int blk = blockIdx.x, nblk = p.nblk;
+  const int n = p.n;
+  const int m = st->m;
+  const int kcap = p.kcap;
+  const int r0 = blk * p.rpb, r1 = min(n, r0 + p.rpb);
+  unsigned long long* bc = &st->bar_count;
+  int* abt = &st->abort_flag;
+  // completed grid barriers of this solve (no barrier is in flight at launch)
+  unsigned long long bar_seen = tid == 0 ? ld_relaxed_gpu64(bc) / (unsigned long long)nblk : 0ull;
+
+  // ---- the previous cycle's recycle update (gcrodr.py:444-467), in place ------
+  // U <- [U | V_0..V_{j-1}] coefU, C <- [C | V_0..V_j] coefC (coefficients of
+  // the dense kernel's P_CYCLE), over this CTA's rows, on the fp64 tensor
+  // cores: DMMA m8n8k4 with A = coef^T (outputs x inputs) and B = the staged
+  // 32-row tile (inputs x rows), so no output padding beyond 8 columns is
+  // wasted. With `partials`, the next cycle start's per-CTA sums C^T r and
+  // |U_c|^2 are formed from the new columns in the same pass.
+  auto apply_update = [&](bool partials) {
+    const int kcp = st->kc_prev, jj = st->j;
+    const int nout = st->upd ? st->k_new : 0;
+    double* part0 = p.part + (size_t)COMB_PART0 * GRID_MAX + blk;
+    if (nout == 0) {  // no update: the next cycle's partials from U, C as they are
+      if (!partials) return;
+      for (int c = 0; c < kcp; ++c) {
+        const double* Cc = colC(p, kcap - kcp + c);
+        const double* Uc = colU(p, c);
+        double s1 = 0.0, s2 = 0.0;
+        for (int row = r0 + tid; row < r1; row += NT) {
+          s1 += Cc[row] * p.r[row];
+          const double u = Uc[row];
+          s2 += u * u;
+        }
+        const double t1 = block_sum(s1, S.bred);
+        const double t2 = block_sum(s2, S.bred);
+        if (tid == 0) {
+          part0[(size_t)c * GRID_MAX] = t1;
+          part0[(size_t)(kcp + c) * GRID_MAX] = t2;
+        }
+      }
+      return;
+    }
+    const int nin_u = kcp + jj, nin_c = kcp + jj + 1;
+    const int ncs = 2 * kcp + jj + 1;  // staged [U (kcp) | C (kcp) | V_0..V_jj], then r
+    const int cld = comb_ld(m);
+    const int kbn = ((nout + 7) >> 3) * 8, nmb = kbn >> 3;  // padded outputs, <= 4 blocks
+    double* stg = cdyn;
+    double* cfs = cdyn + p.sm_cmb;
+    for (int e = tid; e < 2 * kbn * cld; e += NT) {  // cfs[(h kbn + q) cld + i] = coef_h[i][q]
+      const int i = e % cld, q = (e / cld) % kbn, h = e / (cld * kbn);
+      cfs[e] = (q < nout && i < (h ? nin_c : nin_u)) ? (h ? st->coefC : st->coefU)[i + q * LDC]
+                                                     : 0.0;
+    }
+    // warp: outputs of U (uc 0) or C (uc 1), rows 8 nbr .. 8 nbr + 7 of a tile
+    const int uc = warp >> 2, nbr = warp & 3, ln = lane >> 2, lk = lane & 3;
+    const int nin = uc ? nin_c : nin_u, nks = (nin + 3) >> 2;
+    const double* cf = cfs + (size_t)(uc * kbn + ln) * cld + lk;  // A: coef^T[8 mb + ln][4 ks + lk]
+    auto scol = [&](int i) -> int {  // staged column of input i (padding clamped)
+      i = min(i, nin - 1);
+      return i < kcp ? (uc ? kcp + i : i) : 2 * kcp + (i - kcp);
+    };
+    auto src_col = [&](int c) -> const double* {
+      return c < kcp ? colU(p, c) : c < 2 * kcp ? colC(p, kcap - kcp + (c - kcp))
+                   : c < ncs ? colV(p, c - 2 * kcp) : p.r;
+    };
+    constexpr int GPF = 8;  // the next tile's first elements, in flight
+    double pf[GPF];
+    const int nel = 32 * (ncs + 1);
+    auto load_tile = [&](int t0) {
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT, row = t0 + (e & 31);
+        if (e < nel) pf[k] = row < r1 ? src_col(e >> 5)[row] : 0.0;
+      }
+    };
+    double psq[4] = {0.0, 0.0, 0.0, 0.0};  // |U_q|^2 (uc 0) or C_q . r (uc 1), this lane's rows
+    if (r0 < r1) load_tile(r0);
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+      __syncthreads();  // the previous tile (and the coefficients) are in place / consumed
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT;
+        if (e < nel) stg[(e >> 5) * GM_LD + (e & 31)] = pf[k];
+      }
+      for (int e = tid + GPF * NT; e < nel; e += NT) {
+        const int row = t0 + (e & 31);
+        stg[(e >> 5) * GM_LD + (e & 31)] = row < r1 ? src_col(e >> 5)[row] : 0.0;
+      }
+      __syncthreads();
+      if (t0 + 32 < r1) load_tile(t0 + 32);
+      double acc[4][2];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
+      for (int ks = 0; ks < nks; ++ks) {
+        const double bf = stg[scol(4 * ks + lk) * GM_LD + 8 * nbr + ln];
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+          if (mb < nmb)
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[mb][0]), "+d"(acc[mb][1])
+                : "d"(cf[(size_t)mb * 8 * cld + 4 * ks]), "d"(bf));
+      }
+      // D[output 8 mb + ln][row 8 nbr + 2 lk + e]
+      const int rl = 8 * nbr + 2 * lk, row = t0 + rl;
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        const int q = 8 * mb + ln;
+        if (mb < nmb && q < nout) {
+          double* dst = uc ? colC(p, kcap - nout + q) : colU(p, q);
+          if (row < r1) dst[row] = acc[mb][0];
+          if (row + 1 < r1) dst[row + 1] = acc[mb][1];
+          if (partials) {
+            if (uc)
+              psq[mb] += acc[mb][0] * stg[ncs * GM_LD + rl] + acc[mb][1] * stg[ncs * GM_LD + rl + 1];
+            else
+              psq[mb] += acc[mb][0] * acc[mb][0] + acc[mb][1] * acc[mb][1];
+          }
+        }
+      }
+    }
+    if (partials) {  // lanes of an output, then the 4 row-block warps, in a fixed order
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 1);
+        psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 2);
+      }
+      __syncthreads();
+      double* red = stg;
+      if (lk == 0)
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb) red[(uc * 4 + nbr) * 32 + 8 * mb + ln] = psq[mb];
+      __syncthreads();
+      for (int e = tid; e < 2 * nout; e += NT) {
+        const int h = e / nout, q = e % nout;  // h 1: C^T r, h 0: |U|^2
+        const double* rq = red + h * 4 * 32 + q;
+        part0[(size_t)(h ? q : nout + q) * GRID_MAX] = ((rq[0] + rq[32]) + rq[64]) + rq[96];
+      }
+    }
+    __syncthreads();
+  };
   if (st->done) {
+    // the look-ahead launch after the final cycle applies that cycle's update
+    // (the next solve's refresh reads U), then leaves
+    if (st->comb_pending) {
+      apply_update(false);
+      if (!grid_sync(bc, abt, nblk, &S.flag, bar_seen)) return;
+      if (blk == 0 && tid == 0) st->comb_pending = 0;
+    }
     if (blk == 0 && tid == 0) st->ran = 0;
     return;
   }
-  const int n = p.n;
   const int kc = st->kc;
   const bool defl = kc > 0;
-  const int m = st->m;
-  const int kcap = p.kcap;
   int budget = st->max_iter - st->iters;
   int s = defl ? max(1, m - kc) : m;
   s = min(s, budget);
   const double abs_tol = st->abs_tol;
   const double beta = st->rnorm;
-  const int r0 = blk * p.rpb, r1 = min(n, r0 + p.rpb);
   double* Qb = colC(p, kcap - kc);  // [C | V_0 ...] contiguous
   constexpr int TR = 32 * R;
   constexpr int CB = R >= 4 ? 4 : 8;         // sweep-1 basis columns per butterfly batch
@@ -787,9 +949,6 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     return op_row(p, sten, xv, row);
   };
   const size_t ld = p.ld;
-  unsigned long long* bc = &st->bar_count;
-  // completed grid barriers of this solve (no barrier is in flight at launch)
-  unsigned long long bar_seen = tid == 0 ? ld_relaxed_gpu64(bc) / (unsigned long long)nblk : 0ull;
   // Through the stencil form the next SpMV reads only rows within
   // max(sx, sxy) of this CTA's own: after sweep 2 a CTA waits for the `halo`
   // neighbour CTAs on each side instead of the whole grid.
@@ -797,12 +956,19 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   unsigned my_ep = tid == 0 ? ld_relaxed_gpu(nbe + blk * 16) : 0u;
   const int halo = sten ? (max(p.sv.sx, p.sv.sxy) + p.rpb - 1) / p.rpb : -1;
   const bool nbsync = halo >= 0 && 2 * halo + 1 < nblk && 2 * halo + 1 <= NT;
-  int* abt = &st->abort_flag;
   // ---- cycle start --------------------------------------------------------
-  const bool comb_part = st->comb_part != 0;
+  const bool pend = st->comb_pending != 0;
+  if (pend) {
+    apply_update(defl);
+    CYCLE_SYNC();  // every CTA has read comb_pending and written its partials
+    if (blk == 0 && tid == 0) st->comb_pending = 0;
+  }
+  // partials: this launch's update (pend), k_project after a refresh
+  // (comb_part 0), or a k_combine (comb_part 1)
+  const bool comb_part = pend || st->comb_part != 0;
   if (defl) {
     reduce_partials(p.part + (comb_part ? (size_t)COMB_PART0 * GRID_MAX : 0), GRID_MAX,
-                    comb_part ? st->comb_nblk : nblk, 0, 2 * kc, S.red);
+                    pend ? nblk : comb_part ? st->comb_nblk : nblk, 0, 2 * kc, S.red);
     if (tid < kc) {
       double u2 = S.red[kc + tid];
       double un = sqrt(u2);
@@ -1757,6 +1923,7 @@ __global__ void __launch_bounds__(NT) k_dense(Ptrs p, int prog, int arg, int cyc
         st->warn |= warn;
         if (r < 0) st->status |= (1 << (-r));
         st->kc_prev = kc;
+        st->comb_pending = 1;
         if (r > 0) {
           st->upd = 1;
           st->k_new = r;
@@ -2008,8 +2175,10 @@ static void release_slot(int i) {
 
 // per-thread pool of timing events (cycle kernel / dense kernel brackets)
 struct EventPool {
+  std::mutex mu;  // several host threads may share a stream's pool
   std::vector<cudaEvent_t> ev;
   cudaEvent_t get(size_t i) {
+    std::lock_guard<std::mutex> lk(mu);
     while (ev.size() <= i) {
       cudaEvent_t e;
       cudaEventCreate(&e);
@@ -2018,6 +2187,9 @@ struct EventPool {
     return ev[i];
   }
 };
+// per-cycle timing events: a ring of EV_RING (cycle, dense) bracket triples;
+// a slot's times are collected before the slot is reused
+constexpr int EV_RING = 16;
 // timing events per stream (reused across solves and host threads: creating
 // CUDA objects in a fresh host thread while other chains' kernels run can
 // stall for a long time)
@@ -2218,6 +2390,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.sm_R = (int)SL.R;
   p.sm_B = (int)SL.B;
   p.sm_csr = (int)SL.csr;
+  p.sm_cmb = (int)SL.cmb;
   const size_t cycle_fixed = SL.csr * sizeof(double);
   size_t csr_cap = 0;
   {
@@ -2286,6 +2459,16 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     release_slot(slot);
     return SKR_ERR_CUDA;
   }
+  double cyc_ms = 0.0, den_ms = 0.0;
+  auto collect = [&](int c2) {  // cycle c2's kernel times (its events are recorded)
+    const size_t sl = 3 * (size_t)(c2 % EV_RING);
+    cudaEventSynchronize(t_events.get(4 + sl));
+    float a = 0.f, b2 = 0.f;
+    cudaEventElapsedTime(&a, t_events.get(2 + sl), t_events.get(3 + sl));
+    cudaEventElapsedTime(&b2, t_events.get(3 + sl), t_events.get(4 + sl));
+    cyc_ms += a;
+    den_ms += b2;
+  };
   // cycles with look-ahead
   const int LOOK = 2;
   int enq = 0, seen = 0;
@@ -2301,18 +2484,19 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     if (vf[1]) break;
     while (enq < seen + LOOK) {
       cyc = enq;
-      cudaEventRecord(t_events.get(2 + 3 * (size_t)enq), s);
+      if (enq >= EV_RING) collect(enq - EV_RING);
+      const size_t slot3 = 3 * (size_t)(enq % EV_RING);
+      cudaEventRecord(t_events.get(2 + slot3), s);
       cudaError_t e =
           cudaLaunchCooperativeKernel(cycle_fn, dim3(nblk), dim3(NT), cargs, cycle_dsmem, s);
       if (e != cudaSuccess) {
         result = SKR_ERR_CUDA;
         break;
       }
-      cudaEventRecord(t_events.get(3 + 3 * (size_t)enq), s);
+      cudaEventRecord(t_events.get(3 + slot3), s);
       k_dense<<<1, NT, dsm, s>>>(p, P_CYCLE, 0, enq);
-      cudaEventRecord(t_events.get(4 + 3 * (size_t)enq), s);
-      launch_combine(kt, p, ncomb, 1, s);
-      launches += 3;
+      cudaEventRecord(t_events.get(4 + slot3), s);
+      launches += 2;  // the update is applied at the start of the next k_cycle
       ++enq;
     }
     if (result) break;
@@ -2360,9 +2544,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     if (vf[1]) break;
     ++seen;
   }
+  // the last cycle's update if no look-ahead k_cycle launch applied it
+  launch_combine(kt, p, ncomb, 1, s);
   k_final_resid<<<nblk, NT, 0, s>>>(p);
   k_dense<<<1, NT, dsm, s>>>(p, P_FINAL, 0, -1);
-  launches += 3;  // incl. k_setup
+  launches += 4;  // incl. k_setup
   cudaEventRecord(ev1, s);
   if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess)
     result = SKR_ERR_CUDA;
@@ -2376,14 +2562,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const State& hs = *reinterpret_cast<const State*>(hbuf.data());
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
-  double cyc_ms = 0.0, den_ms = 0.0;
-  for (int c2 = 0; c2 < enq; ++c2) {
-    float a = 0.f, b2 = 0.f;
-    cudaEventElapsedTime(&a, t_events.get(2 + 3 * (size_t)c2), t_events.get(3 + 3 * (size_t)c2));
-    cudaEventElapsedTime(&b2, t_events.get(3 + 3 * (size_t)c2), t_events.get(4 + 3 * (size_t)c2));
-    cyc_ms += a;
-    den_ms += b2;
-  }
+  for (int c2 = std::max(0, enq - EV_RING); c2 < enq; ++c2) collect(c2);
   if (hs.abort_flag) return SKR_ERR_TIMEOUT;
   memset(rep, 0, sizeof(*rep));
   rep->iterations = hs.iters;
@@ -2436,7 +2615,7 @@ int skr_gcrodr_solve_chains(const skr_system* systems, const int32_t* chain_firs
   if (int rc0 = chain_streams(dev, n_chains, streams)) return rc0;
   for (int c = 0; c < n_chains; ++c) {  // event pools up front, on this thread
     EventPool& ep = event_pool(streams[c]);
-    ep.get(2 + 3 * 64);
+    ep.get(2 + 3 * EV_RING);
   }
   std::vector<int> status(n_chains, SKR_OK);
   auto run_chain = [&](int c) {
@@ -2522,7 +2701,8 @@ int skr_dense_hr_first(const double* H, int32_t ldh, int32_t m, int32_t k, doubl
   cudaMemcpyAsync(hout, dout, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(dout, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return SKR_ERR_CUDA;
-  *ncols = hout[0];
+  ncols[0] = hout[0];
+  ncols[1] = hout[1];
   return SKR_OK;
 }
 
@@ -2543,7 +2723,8 @@ int skr_dense_hr_next(const double* G, int32_t ldg, const double* cross, int32_t
   cudaMemcpyAsync(hout, dout, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(dout, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return SKR_ERR_CUDA;
-  *ncols = hout[0];
+  ncols[0] = hout[0];
+  ncols[1] = hout[1];
   return SKR_OK;
 }
 

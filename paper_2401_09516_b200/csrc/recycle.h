@@ -115,9 +115,70 @@ SKR_HD int hr_first(const Ctx& c, Arena& ar, const double* H, int ldh, int m, in
     }
   }
   if (singular) {
-    // reference: generalized problem (H^T H + h^2 e e^T, H^T) via QZ -- not ported
+    // gcrodr.py:196-203: the generalized problem (H^T H + h^2 e e^T) z =
+    // theta H^T z (the reference: QZ, scipy eig(lhs, H^T)). Solved here as the
+    // ordinary problem of (A - sigma H^T)^-1 H^T, A = H^T H + h^2 e e^T, whose
+    // eigenvalues are nu = 1 / (theta - sigma) with the same eigenvectors; the
+    // pencil's infinite eigenvalues (H^T singular) become nu = 0 and are never
+    // among the k smallest |theta|; the selection runs on theta = sigma + 1/nu.
+    // sigma = 0 unless A is singular or badly conditioned (a null vector of H
+    // orthogonal to e_m makes theta = 0 an eigenvalue), then small shifts.
     *warn |= W_SINGULAR_H;
-    return -D_UNSUPPORTED;
+    const double h2 = hsub * hsub;
+    double sigma = 0.0;
+    bool ok = false;
+    for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+      gemm(c, true, ar.M1, ar.ld, ar.M1, ar.ld, ar.M2, ar.ld, m, m, m);  // Hs^T Hs
+      bsync();
+      if (attempt > 0) {
+        const double an = fro_norm(c, ar.M2, ar.ld, m, m, ar.red) + h2;
+        const double fac[3] = {1.0e-3, -7.3e-3, 3.1e-2};
+        sigma = fac[attempt - 1] * an / (fn > 0.0 ? fn : 1.0);
+      }
+      for (Flat2 f_(c, m, m); f_.ok(); f_.next()) {
+        const int i = f_.i, j = f_.j;
+        DA(ar.M2, ar.ld, i, j) -= sigma * DA(ar.M1, ar.ld, j, i);  // - sigma H^T
+        DA(ar.M4, ar.ld, i, j) = DA(ar.M1, ar.ld, j, i);            // H^T
+      }
+      bsync();
+      if (c.tid == 0) DA(ar.M2, ar.ld, m - 1, m - 1) += h2;
+      bsync();
+      const double an2 = fro_norm(c, ar.M2, ar.ld, m, m, ar.red);
+      int info2 = 0;
+      lu_factor(c, ar.M2, ar.ld, m, piv, &info2);
+      if (info2 != 0) continue;
+      // conditioning certificate ||S||_F ||S^-1||_F from S^-1 (identity RHS in M3)
+      for (Flat2 f_(c, m, m); f_.ok(); f_.next())
+        DA(ar.M3, ar.ld, f_.i, f_.j) = f_.i == f_.j ? 1.0 : 0.0;
+      bsync();
+      lu_solve(c, ar.M2, ar.ld, m, piv, ar.M3, ar.ld, m);
+      const double gn2 = fro_norm(c, ar.M3, ar.ld, m, m, ar.red);
+      if (!(an2 * gn2 < KAPPA_CERT)) continue;
+      lu_solve(c, ar.M2, ar.ld, m, piv, ar.M4, ar.ld, m);  // M4 = (A - sigma H^T)^-1 H^T
+      bsync();
+      ok = true;
+    }
+    if (!ok) return -D_LINALG_ERROR;
+    double* wr = ar.vec;
+    double* wi = ar.vec + ar.ld;
+    // Z log in M2 (the LU factors of A are dead)
+    if (eig_schur(c, ar.M4, ar.ld, m, ar.M3, ar.ld, wr, wi, ar.vec + 2 * ar.ld, ar.M2,
+                  ar.ld * ar.ld / ZREC) != 0)
+      return -D_QR_NOCONV;
+    double* kr = ar.vec + 9 * ar.ld;  // theta = sigma + 1 / nu (inf for nu = 0)
+    double* ki = ar.vec + 10 * ar.ld;
+    for (int i = c.tid; i < m; i += c.nt) {
+      const double d2 = wr[i] * wr[i] + wi[i] * wi[i];
+      kr[i] = d2 > 0.0 ? sigma + wr[i] / d2 : INFINITY;
+      ki[i] = d2 > 0.0 ? -wi[i] / d2 : 0.0;
+    }
+    bsync();
+    int ncols = select_basis(c, ar.M4, ar.ld, m, ar.M3, ar.ld, wr, wi, kk, m, ar.M1, ar.ld,
+                             ar.iw + ar.ld, ar.xwork, ar.red, kr, ki);
+    if (ncols < 0) return -D_LINALG_ERROR;
+    int* jp = ar.iw + 6 * ar.ld;
+    return qrcp(c, ar.M1, ar.ld, m, ncols, jp, ar.M2, ar.ld, RANK_RTOL, ar.vec + 2 * ar.ld,
+                ar.vec + 5 * ar.ld);
   }
   // modified = Hs + h^2 f e_m^T
   double h2 = hsub * hsub;

@@ -316,10 +316,11 @@ def harmonic_ritz_first_cycle(H_m, h_sub: float, k: int):
     Hb[m, m - 1] = h_sub
     Hd = torch.from_numpy(np.asfortranarray(Hb).T.copy()).to("cuda")  # column-major
     P = torch.zeros((m + 2, m), dtype=torch.float64, device="cuda")
-    nc = ctypes.c_int32()
+    nc = (ctypes.c_int32 * 2)()
     _lib.check(L.skr_dense_hr_first(Hd.data_ptr(), m + 1, m, int(k), P.data_ptr(), m,
-                                    ctypes.byref(nc), _lib.stream_handle()), "hr_first")
-    r = nc.value
+                                    nc, _lib.stream_handle()), "hr_first")
+    r = nc[0]
+    _emit_warnings(nc[1] & (_lib.WARN_SINGULAR_H | _lib.WARN_SINGULAR_CROSS))
     if r < 0:
         raise np.linalg.LinAlgError(f"device harmonic Ritz failed (status {-r})")
     flat = P.cpu().numpy().ravel()[: m * r]
@@ -342,11 +343,12 @@ def harmonic_ritz_subsequent(G, W_r_V, k: int):
     Gd = torch.from_numpy(np.ascontiguousarray(G.T)).to("cuda")
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to("cuda")
     P = torch.zeros((mm + 2, mm), dtype=torch.float64, device="cuda")
-    nc = ctypes.c_int32()
+    nc = (ctypes.c_int32 * 2)()
     _lib.check(L.skr_dense_hr_next(Gd.data_ptr(), mm + 1, Xd.data_ptr(), mm, mm, int(k),
-                                   P.data_ptr(), mm, ctypes.byref(nc), _lib.stream_handle()),
+                                   P.data_ptr(), mm, nc, _lib.stream_handle()),
                "hr_next")
-    r = nc.value
+    r = nc[0]
+    _emit_warnings(nc[1] & (_lib.WARN_SINGULAR_H | _lib.WARN_SINGULAR_CROSS))
     if r < 0:
         raise np.linalg.LinAlgError(f"device harmonic Ritz failed (status {-r})")
     flat = P.cpu().numpy().ravel()[: mm * r]

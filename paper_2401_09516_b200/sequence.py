@@ -29,7 +29,7 @@ from .gmres import SolverConfig
 from .sparse import DeviceCsr
 
 __all__ = ["SequenceResult", "ChainState", "solve_sequence", "solve_chains", "chunk_positions",
-           "split_chunks"]
+           "split_chunks", "gather_results"]
 
 
 @dataclass
@@ -364,3 +364,36 @@ def _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states, g
         print(f"trace py prep {1e3 * (t0 - t_enter):.2f} ms native {1e3 * wall:.2f} ms "
               f"post {1e3 * (time.perf_counter() - t_native_end):.2f} ms", file=_sys.stderr)
     return out
+
+
+def gather_results(results: Sequence, positions: Sequence, group=None, dst: int = 0,
+                   with_x: bool = True):
+    """Collect every rank's chain results (this rank's ``results[i]`` solved
+    the sorted ``positions[i]``) on rank ``dst`` in sorted-position order: the
+    one collective of the multi-GPU path, after the solves.
+    Returns a dict (positions, order, iterations, converged, true_rel,
+    warn_bits, x) on ``dst`` and None elsewhere; x is gathered as host arrays
+    (numpy), ``with_x=False`` skips it. Works on NCCL and gloo groups (object
+    collectives)."""
+    import torch.distributed as dist
+
+    rows = []
+    for r, pos in zip(results, positions):
+        for q, p_ in enumerate(pos):
+            x = None
+            if with_x and q < len(r.x):
+                x = r.x[q]
+                x = x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+            rows.append((int(p_), int(r.order[q]), int(r.iterations[q]), bool(r.converged[q]),
+                         float(r.true_rel[q]) if q < len(r.true_rel) else float("nan"),
+                         int(r.warn_bits[q]) if q < len(r.warn_bits) else 0, x))
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        out = [None] * world if rank == dst else None
+        dist.gather_object(rows, out, dst=dst, group=group)
+        if rank != dst:
+            return None
+        rows = [row for part in out for row in part]
+    rows.sort(key=lambda t: t[0])
+    keys = ("positions", "order", "iterations", "converged", "true_rel", "warn_bits", "x")
+    return {k: [row[i] for row in rows] for i, k in enumerate(keys)}

@@ -175,32 +175,62 @@ def gather_distance_rows(local, n_sys: int, group=None):
     return torch.cat(chunks)[:n_sys].contiguous()
 
 
-def sharded_greedy_sort(flat_dev, group=None, stream=None) -> list[int]:
-    """Multi-GPU greedy sort: D2 rows sharded by rank, NCCL all_gather, then the
-    (deterministic, replicated) chain on every rank. Every rank holds all params."""
-    import torch
+class _DeviceSortKernels:
+    """The C-ABI kernels behind sharded_greedy_sort (skr_sort_binary_check,
+    skr_sort_dist2, skr_sort_chain). Tests substitute host stand-ins to
+    exercise the multi-rank control flow on CPU (gloo)."""
+
+    def __init__(self, stream=None):
+        self.sh = _lib.stream_handle(stream)
+        self.L = _lib.load()
+
+    def prepare(self, flat):
+        n_sys, P = flat.shape
+        self.ws, self.need = _SortWorkspace.get(n_sys, P)
+        v = np.zeros(2)
+        isb = ctypes.c_int32()
+        _lib.check(self.L.skr_sort_binary_check(flat.data_ptr(), n_sys, P, v.ctypes.data,
+                                                ctypes.byref(isb), self.ws.data_ptr(), self.need,
+                                                self.sh), "binary_check")
+        self.isb, self.v = isb.value, v
+
+    def dist2_rows(self, flat, r0, r1):
+        import torch
+
+        n_sys, P = flat.shape
+        local = torch.zeros((max(r1 - r0, 0), n_sys), dtype=torch.float64, device="cuda")
+        if r1 > r0:
+            _lib.check(self.L.skr_sort_dist2(flat.data_ptr(), n_sys, P, r0, r1, self.isb,
+                                             float(self.v[0]), float(self.v[1]), local.data_ptr(),
+                                             self.ws.data_ptr(), self.need, self.sh), "dist2")
+        return local
+
+    def chain(self, D2, flat):
+        import torch
+
+        n_sys, P = flat.shape
+        order = torch.zeros(n_sys, dtype=torch.int32, device="cuda")
+        ncert = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(self.L.skr_sort_chain(D2.data_ptr(), flat.data_ptr(), n_sys, P, self.isb,
+                                         order.data_ptr(), ncert.data_ptr(), self.sh), "chain")
+        return [int(i) for i in order.cpu()]
+
+
+def sharded_greedy_sort(flat_dev, group=None, stream=None, kernels=None) -> list[int]:
+    """Multi-GPU greedy sort (sorting.py:55-80 over N ranks): rank r computes
+    the squared-distance rows row_shard(n, N, r) (skr_sort_dist2), the row
+    blocks are all-gathered (NCCL over NVLink on the GPU box), and every rank
+    runs the same deterministic chain (skr_sort_chain, lowest-index ties)
+    on the full matrix. Every rank holds all parameters."""
     import torch.distributed as dist
 
-    L = _lib.load()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    n_sys, P = flat_dev.shape
+    n_sys = flat_dev.shape[0]
     flat_dev = flat_dev.contiguous()
-    ws, need = _SortWorkspace.get(n_sys, P)
-    sh = _lib.stream_handle(stream)
-    v = np.zeros(2)
-    isb = ctypes.c_int32()
-    _lib.check(L.skr_sort_binary_check(flat_dev.data_ptr(), n_sys, P, v.ctypes.data,
-                                       ctypes.byref(isb), ws.data_ptr(), need, sh), "binary_check")
+    k = kernels if kernels is not None else _DeviceSortKernels(stream)
+    k.prepare(flat_dev)
     r0, r1 = row_shard(n_sys, world, rank)
-    local = torch.zeros((max(r1 - r0, 0), n_sys), dtype=torch.float64, device="cuda")
-    if r1 > r0:
-        _lib.check(L.skr_sort_dist2(flat_dev.data_ptr(), n_sys, P, r0, r1, isb.value,
-                                    float(v[0]), float(v[1]), local.data_ptr(), ws.data_ptr(),
-                                    need, sh), "dist2")
+    local = k.dist2_rows(flat_dev, r0, r1)
     D2 = gather_distance_rows(local, n_sys, group)
-    order = torch.zeros(n_sys, dtype=torch.int32, device="cuda")
-    ncert = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.check(L.skr_sort_chain(D2.data_ptr(), flat_dev.data_ptr(), n_sys, P, isb.value,
-                                order.data_ptr(), ncert.data_ptr(), sh), "chain")
-    return [int(i) for i in order.cpu()]
+    return k.chain(D2, flat_dev)

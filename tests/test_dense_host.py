@@ -195,3 +195,28 @@ def test_cholqr2_orthonormal_and_rank(H):
     assert r == Qr.shape[1] == 6
     np.testing.assert_allclose(Q[:, :r].T @ Q[:, :r], np.eye(r), atol=1e-13)
     assert span_dist(Q[:, :r], Qr) < 1e-10
+
+
+def test_harmonic_ritz_first_singular_h_golden(H):
+    """Singular / nearly singular Hessenberg (sigma_min < 1e-14 sigma_max):
+    the reference's generalized fallback (gcrodr.py:189-203, QZ on
+    (H^T H + h^2 e e^T, H^T)) against its own outputs; the device solves the
+    inverse problem of A^-1 H^T and selects on theta = 1 / mu, with the
+    reference's warning bit."""
+    d = np.load(os.path.join(GOLD, "dense_singular.npz"))
+    t = 0
+    while f"s{t}_H" in d:
+        Hs = d[f"s{t}_H"]
+        m = Hs.shape[0]
+        Hf = np.zeros((m + 1, m), order="F")
+        Hf[:m] = Hs
+        Hf[m, m - 1] = float(d[f"s{t}_h"])
+        P = np.zeros((m, m), order="F")
+        w = ctypes.c_int(0)
+        r = H.skrh_hr_first(dp(Hf), m + 1, m, int(d[f"s{t}_k"]), dp(P), m, ctypes.byref(w))
+        ref = d[f"s{t}_P"]
+        assert w.value & 1, t  # W_SINGULAR_H
+        assert r == ref.shape[1], (t, r, ref.shape)
+        assert span_dist(P[:, :r], ref) < 1e-8, (t, span_dist(P[:, :r], ref))
+        t += 1
+    assert t == 4

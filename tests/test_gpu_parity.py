@@ -287,6 +287,22 @@ def test_dense_harmonic_ritz_golden():
         assert _span_dist(P, d[f"hs{t}_P"]) < 1e-8 + 1e-12 * cond
 
 
+def test_harmonic_ritz_first_singular_h_golden():
+    """The first-cycle fallback for a singular Hessenberg (gcrodr.py:189-203:
+    sigma_min < 1e-14 sigma_max -> eig(H^T H + h^2 e e^T, H^T), with the
+    reference's warning) on the device vs the reference's own outputs."""
+    skr = _skr()
+    d = np.load(os.path.join(GOLD, "dense_singular.npz"))
+    for t in range(4):
+        H = d[f"s{t}_H"]
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            P = skr.harmonic_ritz_first_cycle(H, float(d[f"s{t}_h"]), int(d[f"s{t}_k"]))
+        assert any("singular Hessenberg" in str(x.message) for x in w), t
+        assert P.shape == d[f"s{t}_P"].shape, t
+        assert _span_dist(P, d[f"s{t}_P"]) < 1e-8, t
+
+
 # ----------------------------------------------------------------------------- solver
 def _chain_fixture(name):
     return np.load(os.path.join(GOLD, f"chain_{name}.npz"))

@@ -42,8 +42,39 @@ def _worker(rank, world, port, q):
         # replicated greedy chain from the gathered matrix == oracle order
         order = orc.greedy_order_from_d2(D2.numpy())
         ok_order = order == orc.greedy_order(flat)
+        # the real sharded_greedy_sort control flow (row shards, padding,
+        # all_gather, replicated chain) with host stand-ins for its kernels
+        from paper_2401_09516_b200.sorting import sharded_greedy_sort
+
+        class HostKernels:
+            def prepare(self, f):
+                pass
+
+            def dist2_rows(self, f, a, b):
+                f = f.numpy()
+                return torch.from_numpy(((f[a:b, None, :] - f[None, :, :]) ** 2).sum(-1))
+
+            def chain(self, D2, f):
+                return orc.greedy_order_from_d2(D2.numpy())
+
+        ok_sharded = sharded_greedy_sort(torch.from_numpy(flat), kernels=HostKernels()) == \
+            orc.greedy_order(flat)
+        # cross-rank gather of per-rank chain results into sorted-position order
+        from paper_2401_09516_b200.sequence import SequenceResult, gather_results
+
+        per = -(-10 // world)
+        mine = [p_ for p_ in range(10) if p_ // per == rank]
+        r = SequenceResult(order=[100 + p_ for p_ in mine], iterations=[p_ * 3 for p_ in mine],
+                           converged=[True] * len(mine), true_rel=[1e-9] * len(mine),
+                           x=[np.full(4, float(p_)) for p_ in mine])
+        g = gather_results([r], [mine])
+        ok_gather_res = (rank != 0) or (
+            g["positions"] == list(range(10)) and g["iterations"] == [p_ * 3 for p_ in range(10)]
+            and g["order"] == [100 + p_ for p_ in range(10)]
+            and all(np.array_equal(x, np.full(4, float(p_))) for p_, x in enumerate(g["x"])))
         pos = list(chunk_positions(1024, world, rank))
-        q.put((rank, ok_gather, ok_order, pos[0], pos[-1], len(pos)))
+        q.put((rank, ok_gather and ok_sharded and ok_gather_res, ok_order, pos[0], pos[-1],
+               len(pos)))
     finally:
         dist.destroy_process_group()
 

@@ -799,18 +799,19 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       return c < kcp ? colU(p, c) : c < 2 * kcp ? colC(p, kcap - kcp + (c - kcp))
                    : c < ncs ? colV(p, c - 2 * kcp) : p.r;
     };
-    constexpr int GPF = 8;  // the next tile's first elements, in flight
-    double pf[GPF];
+    constexpr int GPF = 8;  // the next two tiles' first elements, in flight
+    double pf[GPF], pf2[GPF];
     const int nel = 32 * (ncs + 1);
-    auto load_tile = [&](int t0) {
+    auto load_tile = [&](double (&dst)[GPF], int t0) {
 #pragma unroll
       for (int k = 0; k < GPF; ++k) {
         const int e = tid + k * NT, row = t0 + (e & 31);
-        if (e < nel) pf[k] = row < r1 ? src_col(e >> 5)[row] : 0.0;
+        if (e < nel) dst[k] = row < r1 ? src_col(e >> 5)[row] : 0.0;
       }
     };
     double psq[4] = {0.0, 0.0, 0.0, 0.0};  // |U_q|^2 (uc 0) or C_q . r (uc 1), this lane's rows
-    if (r0 < r1) load_tile(r0);
+    if (r0 < r1) load_tile(pf, r0);
+    if (r0 + 32 < r1) load_tile(pf2, r0 + 32);
     for (int t0 = r0; t0 < r1; t0 += 32) {
       __syncthreads();  // the previous tile (and the coefficients) are in place / consumed
 #pragma unroll
@@ -823,7 +824,9 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         stg[(e >> 5) * GM_LD + (e & 31)] = row < r1 ? src_col(e >> 5)[row] : 0.0;
       }
       __syncthreads();
-      if (t0 + 32 < r1) load_tile(t0 + 32);
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) pf[k] = pf2[k];
+      if (t0 + 64 < r1) load_tile(pf2, t0 + 64);
       double acc[4][2];
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
@@ -1492,16 +1495,17 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 #pragma unroll
       for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
     double* xpart = cdyn + p.sm_R - NT;  // last NT doubles of the Gram region
-    constexpr int GPF = 8;               // next tile's first elements, in flight
-    double pf[GPF];
-    auto load_tile = [&](int t0) {
+    constexpr int GPF = 8;               // the next two tiles' first elements, in flight
+    double pf[GPF], pf2[GPF];
+    auto load_tile = [&](double (&dst)[GPF], int t0) {
 #pragma unroll
       for (int k = 0; k < GPF; ++k) {
         const int e = tid + k * NT, row = t0 + (e & 31);
-        if (e < 32 * ncs) pf[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+        if (e < 32 * ncs) dst[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
       }
     };
-    if (r0 < r1) load_tile(r0);
+    if (r0 < r1) load_tile(pf, r0);
+    if (r0 + 32 < r1) load_tile(pf2, r0 + 32);
     for (int t0 = r0; t0 < r1; t0 += 32) {
 #pragma unroll
       for (int k = 0; k < GPF; ++k) {
@@ -1513,7 +1517,9 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         gtile[(e >> 5) * GL + (e & 31)] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
       }
       __syncthreads();
-      if (t0 + 32 < r1) load_tile(t0 + 32);
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) pf[k] = pf2[k];
+      if (t0 + 64 < r1) load_tile(pf2, t0 + 64);
       // warp 0 fetches this tile's x now: its latency hides behind the DMMAs
       const double xold = (tid < 32 && t0 + tid < r1) ? p.x[t0 + tid] : 0.0;
       {  // x update partials: warp w sums the [U | V] columns c == w (mod NW)

@@ -1495,17 +1495,16 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 #pragma unroll
       for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
     double* xpart = cdyn + p.sm_R - NT;  // last NT doubles of the Gram region
-    constexpr int GPF = 8;               // the next two tiles' first elements, in flight
-    double pf[GPF], pf2[GPF];
-    auto load_tile = [&](double (&dst)[GPF], int t0) {
+    constexpr int GPF = 8;               // next tile's first elements, in flight
+    double pf[GPF];
+    auto load_tile = [&](int t0) {
 #pragma unroll
       for (int k = 0; k < GPF; ++k) {
         const int e = tid + k * NT, row = t0 + (e & 31);
-        if (e < 32 * ncs) dst[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+        if (e < 32 * ncs) pf[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
       }
     };
-    if (r0 < r1) load_tile(pf, r0);
-    if (r0 + 32 < r1) load_tile(pf2, r0 + 32);
+    if (r0 < r1) load_tile(r0);
     for (int t0 = r0; t0 < r1; t0 += 32) {
 #pragma unroll
       for (int k = 0; k < GPF; ++k) {
@@ -1517,9 +1516,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         gtile[(e >> 5) * GL + (e & 31)] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
       }
       __syncthreads();
-#pragma unroll
-      for (int k = 0; k < GPF; ++k) pf[k] = pf2[k];
-      if (t0 + 64 < r1) load_tile(pf2, t0 + 64);
+      if (t0 + 32 < r1) load_tile(t0 + 32);
       // warp 0 fetches this tile's x now: its latency hides behind the DMMAs
       const double xold = (tid < 32 && t0 + tid < r1) ? p.x[t0 + tid] : 0.0;
       {  // x update partials: warp w sums the [U | V] columns c == w (mod NW)

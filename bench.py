@@ -53,10 +53,11 @@ sys.path.insert(0, ROOT)
 METRIC = "linear systems solved/sec to rel-res 1e-8 (fp64)"
 NOMINAL_HBM_GBS = 8000.0  # BASELINE.json: "SpMV+ortho HBM GB/s vs 8 TB/s"
 
-# per-config defaults: (chains per GPU, systems per step). Measured on B200
-# (tools/gpu_sweep_c3.sh): C3 8 chains 5.75 systems/s, 4: 5.68, 2: 5.49,
-# 1: 5.17; C4 8: 1.05, 1: 0.94; C1 8 x 64 CTAs.
-DEFAULTS = {0: (8, 16), 1: (8, 16), 2: (8, 8), 3: (8, 8), 4: (8, 8)}
+# per-config defaults: (chains per GPU, systems per step, CTAs per chain or
+# None = chain_grid_ctas). Measured on B200: C3 8 x 37
+# CTAs (every chain's kernel co-resident: 296 = 2 per SM) 6.26 systems/s,
+# 8 x 64 5.95, 4 x 74 6.15, 12 x 48 6.12, 16 x 32 5.71; C1 8 x 64.
+DEFAULTS = {0: (8, 16, None), 1: (8, 16, None), 2: (8, 8, None), 3: (8, 8, 37), 4: (8, 8, 37)}
 
 
 def _args():
@@ -82,8 +83,10 @@ def _args():
     ap.add_argument("--ref-step-s", type=float, default=25.0,
                     help="CPU seconds per step of the --impl reference arm")
     a = ap.parse_args()
-    ch, st = DEFAULTS.get(a.config, (8, 16))
-    a.chains = ch if a.chains is None else a.chains
+    ch, st, ct = DEFAULTS.get(a.config, (8, 16, None))
+    if a.chains is None:  # the CTA default belongs to the default chain count
+        a.chains = ch
+        a.ctas_per_chain = ct if a.ctas_per_chain is None else a.ctas_per_chain
     a.stripe = st if a.stripe is None else a.stripe
     return a
 

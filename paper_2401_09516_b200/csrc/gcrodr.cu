@@ -162,6 +162,8 @@ struct Ptrs {
   double* hist;
   double* checks;
   int n, ld, kcap, nblk, rpb;
+  int fuse_comb;  // 1: k_cycle applies the recycle update at its start (large row slices);
+                  // 0: a separate k_combine launch after every dense update
 };
 
 __device__ __forceinline__ double* colU(const Ptrs& p, int c) { return p.basis + (size_t)c * p.ld; }
@@ -439,9 +441,10 @@ template <int KT>
 __global__ void __launch_bounds__(NT, 2) k_combine(Ptrs p, int cycle_mode) {
   State* st = p.st;
   if (cycle_mode) {
-    // the last cycle's update when no k_cycle launch applied it (k_cycle
-    // clears the flag after applying it; the next solve's k_setup resets it)
-    if (!st->comb_pending) return;
+    // fused mode: only the last cycle's update when no k_cycle launch applied
+    // it (k_cycle clears the flag after applying it; k_setup resets it);
+    // otherwise after every dense update that followed a cycle
+    if (p.fuse_comb ? !st->comb_pending : !st->ran) return;
   } else if (st->done) {
     return;
   }
@@ -679,6 +682,7 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
 constexpr double V0_PROJ_RTOL = 1e-6;
 
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
+constexpr int FUSE_COMB_ROWS = 4096;  // rows per CTA from which k_cycle applies the update
 constexpr int GM_LD = 36;  // the same for the DMMA Gram (== 4 mod 16: conflict-free fragments)
 
 // k_cycle dynamic shared memory, sized by (m, kcap) (offsets in doubles):
@@ -881,7 +885,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   if (st->done) {
     // the look-ahead launch after the final cycle applies that cycle's update
     // (the next solve's refresh reads U), then leaves
-    if (st->comb_pending) {
+    if (p.fuse_comb && st->comb_pending) {
       apply_update(false);
       if (!grid_sync(bc, abt, nblk, &S.flag, bar_seen)) return;
       if (blk == 0 && tid == 0) st->comb_pending = 0;
@@ -960,7 +964,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   const int halo = sten ? (max(p.sv.sx, p.sv.sxy) + p.rpb - 1) / p.rpb : -1;
   const bool nbsync = halo >= 0 && 2 * halo + 1 < nblk && 2 * halo + 1 <= NT;
   // ---- cycle start --------------------------------------------------------
-  const bool pend = st->comb_pending != 0;
+  const bool pend = p.fuse_comb && st->comb_pending != 0;
   if (pend) {
     apply_update(defl);
     CYCLE_SYNC();  // every CTA has read comb_pending and written its partials
@@ -2385,6 +2389,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const int nblk = cfg_nblk(*d, n, cfg->grid_ctas);
   p.nblk = nblk;
   p.rpb = (int)align_up((size_t)((n + nblk - 1) / nblk), 32);
+  // the in-kernel (tensor-core) recycle update pays off when the row slices
+  // are long; with short ones (C1 at 64 CTAs: 1,024 rows) a separate
+  // k_combine on every SM has the lower latency (measured: C1 -5% fused)
+  p.fuse_comb = p.rpb >= FUSE_COMB_ROWS ? 1 : 0;
+  if (const char* e = getenv("SKR_FUSE_COMB")) p.fuse_comb = atoi(e) ? 1 : 0;
   const int kt = L.kcap;
   const int k_eff = cfg->k == 0 ? 0 : k_in;
   // CSR slice cache: sized from the mean row length with headroom; CTAs whose
@@ -2499,7 +2508,12 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
       cudaEventRecord(t_events.get(3 + slot3), s);
       k_dense<<<1, NT, dsm, s>>>(p, P_CYCLE, 0, enq);
       cudaEventRecord(t_events.get(4 + slot3), s);
-      launches += 2;  // the update is applied at the start of the next k_cycle
+      launches += 2;
+      // fused: the update is applied at the start of the next k_cycle
+      if (!p.fuse_comb) {
+        launch_combine(kt, p, ncomb, 1, s);
+        ++launches;
+      }
       ++enq;
     }
     if (result) break;
@@ -2548,10 +2562,10 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     ++seen;
   }
   // the last cycle's update if no look-ahead k_cycle launch applied it
-  launch_combine(kt, p, ncomb, 1, s);
+  if (p.fuse_comb) launch_combine(kt, p, ncomb, 1, s);
   k_final_resid<<<nblk, NT, 0, s>>>(p);
   k_dense<<<1, NT, dsm, s>>>(p, P_FINAL, 0, -1);
-  launches += 4;  // incl. k_setup
+  launches += 3 + p.fuse_comb;  // incl. k_setup
   cudaEventRecord(ev1, s);
   if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess)
     result = SKR_ERR_CUDA;

@@ -56,8 +56,9 @@ NOMINAL_HBM_GBS = 8000.0  # BASELINE.json: "SpMV+ortho HBM GB/s vs 8 TB/s"
 # per-config defaults: (chains per GPU, systems per step, CTAs per chain or
 # None = chain_grid_ctas). Measured on B200: C3 8 x 37
 # CTAs (every chain's kernel co-resident: 296 = 2 per SM) 6.26 systems/s,
-# 8 x 64 5.95, 4 x 74 6.15, 12 x 48 6.12, 16 x 32 5.71; C1 8 x 64.
-DEFAULTS = {0: (8, 16, None), 1: (8, 16, None), 2: (8, 8, None), 3: (8, 8, 37), 4: (8, 8, 37)}
+# 8 x 64 5.95, 4 x 74 6.15, 12 x 48 6.12, 16 x 32 5.71; C4 4 x 74 1.14 (8 x 37
+# 1.03, 2 x 148 1.13); C1 8 x 64.
+DEFAULTS = {0: (8, 16, None), 1: (8, 16, None), 2: (8, 8, None), 3: (8, 8, 37), 4: (4, 8, 74)}
 
 
 def _args():

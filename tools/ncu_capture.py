@@ -3,7 +3,7 @@ of config CID (warm-up, recycle space), then system 1 inside the NVTX range
 "capture" with the per-chain CTA count of the bench (chain_grid_ctas(chains)).
 Prints the capture solve's algorithmic SpMV+ortho bytes and k_cycle launches
 (SURVEY 8(d)), the denominators of the DRAM/algorithmic ratio.
-usage: python tools/ncu_capture.py CID [CHAINS]"""
+usage: python tools/ncu_capture.py CID [CTAS_PER_CHAIN]"""
 import json
 import os
 import sys
@@ -15,12 +15,12 @@ import paper_2401_09516_b200 as skr  # noqa: E402
 from paper_2401_09516_b200 import problems as P  # noqa: E402
 
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-chains = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+ctas = int(sys.argv[2]) if len(sys.argv) > 2 else 37
 spec = P.CONFIGS[cid]
 cfg = skr.SolverConfig(m=spec.m, k=spec.k, tol=spec.tol, max_iter=spec.max_iter)
 systems = [P.assemble_device(spec, i)[:2] for i in range(2)]
 torch.cuda.synchronize()
-g = skr.chain_grid_ctas(chains)
+g = ctas
 r0 = skr.solve_sequence(systems, [0], cfg, spec.precond, keep_x="none", grid_ctas=g)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("capture")

@@ -66,7 +66,12 @@ typedef struct skr_config {
                         Callers running several chains concurrently on one GPU
                         give each chain a share (e.g. 2 * SMs / chains * 2). */
   double tol;
+  int32_t flags;     /* SKR_COLLECT_DIAGNOSTICS: log (stage, k, ||op U - C||_F,
+                        ||C^T C - I||_F) after the refresh and after every deflated
+                        cycle's recycle update, read with skr_gcrodr_diagnostics */
 } skr_config;
+
+enum skr_config_flags { SKR_COLLECT_DIAGNOSTICS = 1 };
 
 /* SolveReport (gmres.py:46-56) minus the vectors. */
 typedef struct skr_report {
@@ -151,6 +156,12 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
                      const skr_config* cfg, const double* U_in, int32_t ldu, int32_t k_in,
                      void* workspace, size_t ws_bytes, skr_report* report, double* hist,
                      int32_t hist_cap, double* checks, int32_t checks_cap, void* stream);
+/* The diagnostics the last solve logged with SKR_COLLECT_DIAGNOSTICS
+ * (gcrodr.py:372-376, :461-467): up to cap records of 4 doubles (stage: 0 =
+ * refresh, 1 = cycle; k; ||op U - C||_F; ||C^T C - I||_F) into out (host).
+ * Returns the number of records (>= 0) or a negative status. */
+int skr_gcrodr_diagnostics(void* workspace, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
+                           int32_t max_iter, double* out, int32_t cap);
 /* Device pointers of the recycle pair left in the workspace by the last solve:
  * U (n x k, ld) and C (n x k, ld). */
 int skr_gcrodr_recycle_view(void* workspace, size_t ws_bytes, int32_t n, int32_t m, int32_t k,

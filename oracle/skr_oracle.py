@@ -416,7 +416,17 @@ class Result:
     info: dict = field(default_factory=dict)
 
 
-def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None, deadline=None) -> Result:
+def recycle_residuals(U, C, op):
+    """(||op U - C||_F, ||C^T C - I||_F) (gcrodr.py:116-123)."""
+    if U is None or U.shape[1] == 0:
+        return 0.0, 0.0
+    opU = np.column_stack([op(U[:, q]) for q in range(U.shape[1])])
+    return (float(np.linalg.norm(opU - C, "fro")),
+            float(np.linalg.norm(C.T @ C - np.eye(C.shape[1]), "fro")))
+
+
+def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None, deadline=None,
+           collect_diagnostics=False) -> Result:
     """GCRO-DR solve with a carried recycle basis (gcrodr.py:295-496).
 
     ``U_in`` is the previous system's recycle U (its C is discarded by the
@@ -444,9 +454,16 @@ def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None, deadline=N
     iters = 0
     U = C = None
     defl = 0
+    cyc_diag = []
+    refreshed = None
     if U_in is not None and np.asarray(U_in).shape[1] > 0:
         U, C = refresh(U_in, op)
         iters += np.asarray(U_in).shape[1]
+        refreshed = (U, C)
+        if collect_diagnostics:  # gcrodr.py:372-376
+            rel, orth = recycle_residuals(U, C, op)
+            cyc_diag.append({"stage": "refresh", "k": 0 if U is None else U.shape[1],
+                             "au_c": rel, "orth": orth})
         if U is not None:
             a = C.T @ r
             x = x + U @ a
@@ -524,11 +541,17 @@ def gcrodr(op: Operator, b, cfg: Cfg, U_in=None, x0=None, trace=None, deadline=N
             if Q.shape[1] > 0:
                 C = Wh @ Q
                 U = (Vh @ P)[:, kept] @ _inv_upper(R)
+        if collect_diagnostics:  # gcrodr.py:461-467
+            rel, orth = recycle_residuals(U, C, op)
+            cyc_diag.append({"stage": "cycle", "k": U.shape[1], "au_c": rel, "orth": orth})
         if brk and not conv:
             break
     true_rel = float(np.linalg.norm(b - S @ x)) / bnorm
     info = {"restart_checks": checks, "deflated_steps": defl,
             "recycle_k": 0 if U is None else U.shape[1]}
+    if collect_diagnostics:
+        info["cycles"] = cyc_diag
+        info["refreshed_space"] = refreshed
     if U is None:
         info["gmres_fallback"] = True
     return Result(x, iters, np.asarray(hist), true_rel, conv,

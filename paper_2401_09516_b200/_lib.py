@@ -20,7 +20,7 @@ EXPORTS = (
     "skr_version", "skr_status_string", "skr_device_info", "skr_spmv", "skr_residual",
     "skr_stencil_bytes", "skr_stencil_build", "skr_assemble_fd",
     "skr_gcrodr_workspace_bytes", "skr_gcrodr_solve", "skr_gcrodr_recycle_view",
-    "skr_gcrodr_profile", "skr_gcrodr_solve_chains",
+    "skr_gcrodr_profile", "skr_gcrodr_solve_chains", "skr_gcrodr_diagnostics",
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
     "skr_greedy_sort", "skr_dense_hr_first", "skr_dense_hr_next",
 )
@@ -42,7 +42,10 @@ class SkrSystem(ctypes.Structure):
 
 class SkrConfig(ctypes.Structure):
     _fields_ = [("m", c_int32), ("k", c_int32), ("max_iter", c_int32),
-                ("grid_ctas", c_int32), ("tol", c_double)]
+                ("grid_ctas", c_int32), ("tol", c_double), ("flags", c_int32)]
+
+
+COLLECT_DIAGNOSTICS = 1
 
 
 class SkrReport(ctypes.Structure):
@@ -87,6 +90,8 @@ def _declare(L):
                                      POINTER(c_void_p), POINTER(c_int32), POINTER(c_int32)],
                                     c_int32),
         "skr_gcrodr_profile": ([P, c_size_t, c_int32, c_int32, c_int32, P], c_int32),
+        "skr_gcrodr_diagnostics": ([P, c_size_t, c_int32, c_int32, c_int32, c_int32, P, c_int32],
+                                   c_int32),
         "skr_gcrodr_solve_chains": ([POINTER(SkrSystem), P, c_int32, POINTER(SkrConfig), P,
                                      c_size_t, P, P, P, POINTER(SkrReport)], c_int32),
         "skr_sort_workspace_bytes": ([c_int32, c_int64], c_size_t),

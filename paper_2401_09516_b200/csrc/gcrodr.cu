@@ -64,6 +64,7 @@ struct State {
   int n, ld, m, k, kcap, max_iter, jacobi, nblk, rpb, k_in, has_x0,
       comb_part,  // cycle-start partials: 0 = rows [0, 2kc) (k_project), 1 = COMB_PART0 rows
       comb_nblk,  // CTAs of the k_combine launch that wrote the COMB_PART0 rows
+      ndiag,         // diagnostics records logged (SKR_COLLECT_DIAGNOSTICS)
       comb_pending;  // P_CYCLE left a recycle update (coefU / coefC) for the next
                      // k_cycle launch (or the final k_combine) to apply
   double tol;
@@ -103,7 +104,7 @@ struct State {
 };
 
 struct Layout {
-  size_t state, basis, r, z, part, sred, hist, checks, total;
+  size_t state, basis, r, z, part, sred, hist, checks, dlog, total;
   int ld, kcap, ncols, hist_cap;
 };
 
@@ -132,6 +133,8 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
   off = align_up(off + (size_t)L.hist_cap * sizeof(double), 256);
   L.checks = off;
   off = align_up(off + (size_t)2 * L.hist_cap * sizeof(double), 256);
+  L.dlog = off;  // diagnostics: 4 doubles per record, one per deflated cycle + refresh
+  off = align_up(off + (size_t)4 * (max_iter + 2) * sizeof(double), 256);
   L.total = off;
   return L;
 }
@@ -161,6 +164,7 @@ struct Ptrs {
   double* sred;  // k_cycle per-step partials: [2 buffers][GRID_MAX CTAs][PV_STEP values]
   double* hist;
   double* checks;
+  double* dlog;
   int n, ld, kcap, nblk, rpb;
   int fuse_comb;  // 1: k_cycle applies the recycle update at its start (large row slices);
                   // 0: a separate k_combine launch after every dense update
@@ -1766,6 +1770,84 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 }
 
 // ---------------------------------------------------------------------------
+// diagnostics (collect_diagnostics, gcrodr.py:116-123, :372-376, :461-467):
+// ||op U - C||_F and ||C^T C - I||_F of the current pair, after the refresh
+// (stage 0) and after every deflated cycle's recycle update (stage 1)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool diag_skip(const State* st, int stage) {
+  if (st->zero_rhs) return true;
+  return stage == 1 && (!st->ran || st->kc_prev == 0);  // GMRES cycles log nothing
+}
+// per-CTA partials: [0] sum (op U_q - C_q)^2, [1 + a kc + b] (C^T C)_ab
+__global__ void __launch_bounds__(NT) k_diag(Ptrs p, int stage) {
+  State* st = p.st;
+  if (diag_skip(st, stage)) return;
+  const int kc = st->kc;
+  __shared__ double tile[32][KMAX + 1];
+  __shared__ double s_red[NW];
+  const int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  const bool sten = sten_ok(p.sv);
+  double res = 0.0;
+  for (int row = r0 + threadIdx.x; row < r1; row += NT) {
+    const double d = p.dg ? __ldg(p.dg + row) : 1.0;
+    for (int q = 0; q < kc; ++q) {
+      double v = op_row(p, sten, colU(p, q), row);
+      if (p.dg) v = __ddiv_rn(v, d);
+      v -= colC(p, p.kcap - kc + q)[row];
+      res += v * v;
+    }
+  }
+  const double tres = block_sum(res, s_red);
+  double acc[2] = {0.0, 0.0};  // kc^2 <= 441 < 2 NT entries
+  for (int t0 = r0; t0 < r1; t0 += 32) {
+    for (int e = threadIdx.x; e < 32 * kc; e += NT) {
+      const int rr = e & 31, c = e >> 5, row = t0 + rr;
+      tile[rr][c] = row < r1 ? colC(p, p.kcap - kc + c)[row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = threadIdx.x + h * NT;
+      if (e < kc * kc) {
+        const int a = e / kc, b = e % kc;
+        double g = 0.0;
+        for (int rr = 0; rr < 32; ++rr) g += tile[rr][a] * tile[rr][b];
+        acc[h] += g;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.part[(size_t)GRAM_PART0 * GRID_MAX + blockIdx.x] = tres;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e = threadIdx.x + h * NT;
+    if (e < kc * kc) p.part[(size_t)(GRAM_PART0 + 1 + e) * GRID_MAX + blockIdx.x] = acc[h];
+  }
+}
+// one CTA: fixed-order sums of the partials, one record appended to the log
+__global__ void __launch_bounds__(NT) k_diag_fin(Ptrs p, int stage) {
+  State* st = p.st;
+  if (diag_skip(st, stage)) return;
+  const int kc = st->kc;
+  __shared__ double red[1 + KMAX * KMAX];
+  reduce_partials(p.part + (size_t)GRAM_PART0 * GRID_MAX, GRID_MAX, p.nblk, 0, 1 + kc * kc, red);
+  if (threadIdx.x == 0) {
+    double o = 0.0;
+    for (int a = 0; a < kc; ++a)
+      for (int b = 0; b < kc; ++b) {
+        const double g = red[1 + a * kc + b] - (a == b ? 1.0 : 0.0);
+        o += g * g;
+      }
+    double* rec = p.dlog + 4 * (size_t)st->ndiag;
+    rec[0] = stage;
+    rec[1] = kc;
+    rec[2] = kc > 0 ? sqrt(red[0]) : 0.0;
+    rec[3] = kc > 0 ? sqrt(o) : 0.0;
+    st->ndiag += 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // the single-CTA dense kernel (programs)
 // ---------------------------------------------------------------------------
 __device__ void set_done(State* st, int cycle) {
@@ -2383,6 +2465,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.sred = (double*)(base + L.sred);
   p.hist = (double*)(base + L.hist);
   p.checks = (double*)(base + L.checks);
+  p.dlog = (double*)(base + L.dlog);
   p.n = n;
   p.ld = L.ld;
   p.kcap = L.kcap;
@@ -2394,6 +2477,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   // k_combine on every SM has the lower latency (measured: C1 -5% fused)
   p.fuse_comb = p.rpb >= FUSE_COMB_ROWS ? 1 : 0;
   if (const char* e = getenv("SKR_FUSE_COMB")) p.fuse_comb = atoi(e) ? 1 : 0;
+  const bool diag = (cfg->flags & SKR_COLLECT_DIAGNOSTICS) != 0;
+  if (diag) p.fuse_comb = 0;  // the update is applied before each record
   const int kt = L.kcap;
   const int k_eff = cfg->k == 0 ? 0 : k_in;
   // CSR slice cache: sized from the mean row length with headroom; CTAs whose
@@ -2466,6 +2551,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     k_project<<<nblk, NT, 0, s>>>(p);
     k_dense<<<1, NT, dsm, s>>>(p, P_PROJ_FIN, 0, -1);
     launches += 21;
+    if (diag) {
+      k_diag<<<nblk, NT, 0, s>>>(p, 0);
+      k_diag_fin<<<1, NT, 0, s>>>(p, 0);
+      launches += 2;
+    }
   }
   if (cudaGetLastError() != cudaSuccess) {
     release_slot(slot);
@@ -2513,6 +2603,11 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
       if (!p.fuse_comb) {
         launch_combine(kt, p, ncomb, 1, s);
         ++launches;
+      }
+      if (diag) {
+        k_diag<<<nblk, NT, 0, s>>>(p, 1);
+        k_diag_fin<<<1, NT, 0, s>>>(p, 1);
+        launches += 2;
       }
       ++enq;
     }
@@ -2691,6 +2786,23 @@ int skr_gcrodr_solve_chains(const skr_system* systems, const int32_t* chain_firs
   for (int c = 0; c < n_chains; ++c)
     if (status[c] != SKR_OK) return status[c];
   return SKR_OK;
+}
+
+int skr_gcrodr_diagnostics(void* ws, size_t ws_bytes, int32_t n, int32_t m, int32_t k,
+                           int32_t max_iter, double* out, int32_t cap) {
+  if (!ws || (!out && cap > 0) || max_iter < 1) return -SKR_ERR_ARG;
+  Layout L = make_layout(n, m, k, max_iter);
+  if (ws_bytes < L.total) return -SKR_ERR_WORKSPACE;
+  const State* st = (const State*)((char*)ws + L.state);
+  int nd = 0;
+  if (cudaMemcpy(&nd, &st->ndiag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -SKR_ERR_CUDA;
+  const int ncopy = std::min(nd, cap);
+  if (ncopy > 0 &&
+      cudaMemcpy(out, (char*)ws + L.dlog, sizeof(double) * 4 * ncopy, cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
+    return -SKR_ERR_CUDA;
+  return nd;
 }
 
 int skr_gcrodr_profile(void* ws, size_t ws_bytes, int32_t n, int32_t m, int32_t k,

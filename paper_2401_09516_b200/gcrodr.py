@@ -242,7 +242,25 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
     if cfg.k > 0 and recycle_in is not None and recycle_in.k > 0:
         Ud, ldu = _colmajor_device(recycle_in.U, n)
         U_ptr, k_in = Ud, int(Ud.shape[1])
-    rep = eng.solve(dA, bt, x, x0t, U_ptr, ldu, k_in, stream=stream)
+    refreshed = None
+    if collect_diagnostics and k_in > 0:
+        # the refreshed pair itself (gcrodr.py:364, diagnostics["refreshed_space"]):
+        # the same solve stopped after the refresh (max_iter = k_in: the
+        # refresh counts k_in iterations, gcrodr.py:363)
+        keep = eng.c_cfg.max_iter
+        eng.c_cfg.max_iter = k_in
+        try:
+            rep0 = eng.solve(dA, bt, x, x0t, U_ptr, ldu, k_in, stream=stream, want_history=False)
+        finally:
+            eng.c_cfg.max_iter = keep
+        Ur, Cr, kr, _ = eng.recycle_views()
+        refreshed = RecycleSpace(Ur.clone(), Cr.clone(), kr, system_id) if not rep0.zero_rhs \
+            else None
+    eng.c_cfg.flags = _lib.COLLECT_DIAGNOSTICS if collect_diagnostics else 0
+    try:
+        rep = eng.solve(dA, bt, x, x0t, U_ptr, ldu, k_in, stream=stream)
+    finally:
+        eng.c_cfg.flags = 0
     _emit_warnings(rep.warn_bits)
     hist = eng.hist[: rep.hist_len].copy()
     checks = [(float(eng.checks[2 * i]), float(eng.checks[2 * i + 1]))
@@ -265,8 +283,20 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
             diag["gmres_fallback"] = True
         out_space = RecycleSpace(U.t().contiguous().t() if k else U,
                                  C.t().contiguous().t() if k else C, k, system_id)
-    if collect_diagnostics and out_space.k > 0:
-        diag["recycle_residuals"] = _recycle_residuals(dA, out_space)
+    if collect_diagnostics:
+        # gcrodr.py:372-376, :461-467, :484-485
+        cap = cfg.max_iter + 2
+        rec = np.zeros(4 * cap)
+        nd = eng.L.skr_gcrodr_diagnostics(eng.ws.data_ptr(), eng.nbytes, n, cfg.m, cfg.k,
+                                          cfg.max_iter, rec.ctypes.data, cap)
+        if nd < 0:
+            _lib.check(-nd, "skr_gcrodr_diagnostics")
+        diag["cycles"] = [{"stage": "refresh" if rec[4 * i] == 0 else "cycle",
+                           "k": int(rec[4 * i + 1]), "au_c": float(rec[4 * i + 2]),
+                           "orth": float(rec[4 * i + 3])} for i in range(min(nd, cap))]
+        diag["refreshed_space"] = refreshed
+        if out_space.k > 0:
+            diag["recycle_residuals"] = _recycle_residuals(dA, out_space)
     if rep.status_bits:
         diag["dense_status_bits"] = int(rep.status_bits)
     report = SolveReport(

@@ -151,4 +151,4 @@ def test_skr_config_has_grid_ctas():
     from paper_2401_09516_b200 import _lib
 
     names = [f[0] for f in _lib.SkrConfig._fields_]
-    assert names == ["m", "k", "max_iter", "grid_ctas", "tol"]
+    assert names == ["m", "k", "max_iter", "grid_ctas", "tol", "flags"]

@@ -611,3 +611,44 @@ def test_c3_eight_chain_shape_converges():
             rel = float(torch.linalg.norm(res_v) / torch.linalg.norm(b / d))
             assert rel <= 1.05 * spec.tol, (i, rel)
             assert 300 <= r.iterations[q] <= 900, (i, r.iterations[q])
+
+
+def test_collect_diagnostics_matches_reference():
+    """collect_diagnostics (gcrodr.py:372-376, :461-467, :484-485): one record
+    after the refresh and after every deflated cycle's recycle update, with
+    the reference's (stage, k) sequence and rounding-level ||op U - C||_F,
+    ||C^T C - I||_F; refreshed_space spans the reference's refreshed pair."""
+    skr = _skr()
+    from oracle import skr_oracle as orc
+
+    spec = _spec(1, n=32)
+    sy = [_system(spec, i) for i in range(2)]
+    cfg = skr.SolverConfig(m=20, k=6, tol=1e-10)
+    ocfg = orc.Cfg(m=20, tol=1e-10, k=6)
+    A0, b0, _ = sy[0]
+    M0 = skr.build_preconditioner(A0, "jacobi")
+    rep0, sp0 = skr.gcrodr_solve(A0, b0, M=M0, cfg=cfg, collect_diagnostics=True)
+    op0 = orc.Operator(A0.row_ptr, A0.col_idx, A0.values, spec.N, True)
+    ref0 = orc.gcrodr(op0, b0, ocfg, collect_diagnostics=True)
+    A1, b1, _ = sy[1]
+    M1 = skr.build_preconditioner(A1, "jacobi")
+    U_in = sp0.U.cpu().numpy()
+    rep1, sp1 = skr.gcrodr_solve(A1, b1, M=M1, cfg=cfg, recycle_in=sp0, collect_diagnostics=True)
+    op1 = orc.Operator(A1.row_ptr, A1.col_idx, A1.values, spec.N, True)
+    ref1 = orc.gcrodr(op1, b1, ocfg, U_in=U_in, collect_diagnostics=True)
+    for rep, ref in ((rep0, ref0), (rep1, ref1)):
+        got, want = rep.diagnostics["cycles"], ref.info["cycles"]
+        assert [(d["stage"], d["k"]) for d in got] == [(d["stage"], d["k"]) for d in want]
+        for d, w in zip(got, want):
+            assert d["au_c"] <= max(100 * w["au_c"], 1e-9), (d, w)
+            assert d["orth"] <= max(100 * w["orth"], 1e-9), (d, w)
+    assert rep0.diagnostics["refreshed_space"] is None
+    rs = rep1.diagnostics["refreshed_space"]
+    Ur, Cr = ref1.info["refreshed_space"]
+    assert rs.k == Ur.shape[1]
+    assert _span_dist(rs.U.cpu().numpy(), Ur) < 1e-8
+    assert _span_dist(rs.C.cpu().numpy(), Cr) < 1e-8
+    # the diagnostics mode does not change the solve
+    rep2, _ = skr.gcrodr_solve(A1, b1, M=M1, cfg=cfg, recycle_in=sp0)
+    assert rep2.iterations == rep1.iterations
+    np.testing.assert_allclose(rep2.x, rep1.x, rtol=0, atol=1e-12 * np.abs(rep1.x).max())

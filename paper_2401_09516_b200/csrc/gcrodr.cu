@@ -146,6 +146,10 @@ static Layout make_layout(int n, int m, int k, int max_iter) {
 // reproducible run to run (no floating-point atomics).
 constexpr int GRAM_PART0 = 16;
 constexpr int COMB_PART0 = GRAM_PART0 + PV_MAX;
+// diagnostics partials (k_diag): inside the cross-Gram rows but past the
+// refresh projection's rows [0, 2 kc] (still live when the refresh record is taken)
+constexpr int DIAG_PART0 = 2 * KMAX + 1;
+static_assert(DIAG_PART0 + 1 + KMAX * KMAX <= COMB_PART0, "diagnostics rows");
 
 struct Ptrs {
   int sm_R, sm_B, sm_csr, sm_cmb;  // k_cycle dynamic smem offsets (doubles), cycle_smem_layout
@@ -166,6 +170,7 @@ struct Ptrs {
   double* checks;
   double* dlog;
   int n, ld, kcap, nblk, rpb;
+  double v0_rtol;  // |C^T r| / beta above which V_0 is formed from r - C C^T r (V0_PROJ_RTOL)
   int fuse_comb;  // 1: k_cycle applies the recycle update at its start (large row slices);
                   // 0: a separate k_combine launch after every dense update
 };
@@ -683,7 +688,7 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
   } while (0)
 
 // |C^T r| / beta above which the cycle forms V_0 from r - C C^T r (cycle start)
-constexpr double V0_PROJ_RTOL = 1e-6;
+constexpr double V0_PROJ_RTOL = 1e-12;
 
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
 constexpr int FUSE_COMB_ROWS = 4096;  // rows per CTA from which k_cycle applies the update
@@ -989,23 +994,24 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   }
   // V_0. The reference takes r / beta as it is (gcrodr.py:412). In exact
   // arithmetic C^T r = 0 at every cycle start (the refresh projection and the
-  // deflated LS both leave r orthogonal to C), but in floating point the
-  // reference's cycle does not remove a C-component of r: its LS right-hand
-  // side [c_r; beta; 0] counts c_r once more than r = beta V_0 holds it, so
-  // the component comes back with flipped sign and grows through the C^T V
-  // Gram terms (measured: |c_r| / beta x2-4 per cycle on some C3 systems,
-  // up to 0.4, then the residual stalls at |c_r| and DCGS2's Pythagorean norm
-  // reports a spurious breakdown). When |c_r| > V0_PROJ_RTOL beta, V_0 is
-  // therefore formed from r - C c_r with its measured norm beta0 (r =
-  // C c_r + beta0 V_0 exactly, [C | V] orthonormal again); the LS keeps the
-  // reference's form [c_r; beta0; 0]. Equal in exact arithmetic (c_r = 0).
+  // deflated LS both leave r orthogonal to C). The reference's sequential
+  // CGS(C) + MGS(V) keeps |C^T r| / beta at 1e-10..1e-7 (measured with the
+  // oracle on C3 system 5); the one-reduction DCGS2 treats [C | V] as
+  // orthonormal and lets the component ride along with the lagged vector, so
+  // it grew x2-4 per cycle (to 0.4 on C3 system 5, whose residual then stalled
+  // at |C^T r| until the Pythagorean norm reported a spurious breakdown) and
+  // C lost orthonormality (||C^T C - I|| 1e-14 -> 1e-7 over 9 cycles). When
+  // |c_r| > V0_PROJ_RTOL beta (rounding level), V_0 is therefore formed from
+  // r - C c_r with its measured norm beta0 (r = C c_r + beta0 V_0 exactly,
+  // [C | V] orthonormal again); the LS keeps the reference's form
+  // [c_r; beta0; 0]. Equal in exact arithmetic (c_r = 0).
   double beta0 = beta;
   bool v0proj = false;
   if (defl) {
     __syncthreads();
     double c2 = 0.0;
     for (int q = 0; q < kc; ++q) c2 = fma(S.cr[q], S.cr[q], c2);  // same order in every CTA
-    v0proj = c2 > (V0_PROJ_RTOL * beta) * (V0_PROJ_RTOL * beta);
+    v0proj = c2 > (p.v0_rtol * beta) * (p.v0_rtol * beta);
   }
   {
     double* V0 = colV(p, 0);
@@ -1778,7 +1784,7 @@ __device__ __forceinline__ bool diag_skip(const State* st, int stage) {
   if (st->zero_rhs) return true;
   return stage == 1 && (!st->ran || st->kc_prev == 0);  // GMRES cycles log nothing
 }
-// per-CTA partials: [0] sum (op U_q - C_q)^2, [1 + a kc + b] (C^T C)_ab
+// per-CTA partials (rows DIAG_PART0..): [0] sum (op U_q - C_q)^2, [1 + a kc + b] (C^T C)_ab
 __global__ void __launch_bounds__(NT) k_diag(Ptrs p, int stage) {
   State* st = p.st;
   if (diag_skip(st, stage)) return;
@@ -1817,11 +1823,11 @@ __global__ void __launch_bounds__(NT) k_diag(Ptrs p, int stage) {
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) p.part[(size_t)GRAM_PART0 * GRID_MAX + blockIdx.x] = tres;
+  if (threadIdx.x == 0) p.part[(size_t)DIAG_PART0 * GRID_MAX + blockIdx.x] = tres;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int e = threadIdx.x + h * NT;
-    if (e < kc * kc) p.part[(size_t)(GRAM_PART0 + 1 + e) * GRID_MAX + blockIdx.x] = acc[h];
+    if (e < kc * kc) p.part[(size_t)(DIAG_PART0 + 1 + e) * GRID_MAX + blockIdx.x] = acc[h];
   }
 }
 // one CTA: fixed-order sums of the partials, one record appended to the log
@@ -1830,7 +1836,7 @@ __global__ void __launch_bounds__(NT) k_diag_fin(Ptrs p, int stage) {
   if (diag_skip(st, stage)) return;
   const int kc = st->kc;
   __shared__ double red[1 + KMAX * KMAX];
-  reduce_partials(p.part + (size_t)GRAM_PART0 * GRID_MAX, GRID_MAX, p.nblk, 0, 1 + kc * kc, red);
+  reduce_partials(p.part + (size_t)DIAG_PART0 * GRID_MAX, GRID_MAX, p.nblk, 0, 1 + kc * kc, red);
   if (threadIdx.x == 0) {
     double o = 0.0;
     for (int a = 0; a < kc; ++a)
@@ -2477,6 +2483,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   // k_combine on every SM has the lower latency (measured: C1 -5% fused)
   p.fuse_comb = p.rpb >= FUSE_COMB_ROWS ? 1 : 0;
   if (const char* e = getenv("SKR_FUSE_COMB")) p.fuse_comb = atoi(e) ? 1 : 0;
+  p.v0_rtol = V0_PROJ_RTOL;
+  if (const char* e = getenv("SKR_V0_RTOL")) p.v0_rtol = atof(e);
   const bool diag = (cfg->flags & SKR_COLLECT_DIAGNOSTICS) != 0;
   if (diag) p.fuse_comb = 0;  // the update is applied before each record
   const int kt = L.kcap;

@@ -254,8 +254,8 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
         finally:
             eng.c_cfg.max_iter = keep
         Ur, Cr, kr, _ = eng.recycle_views()
-        refreshed = RecycleSpace(Ur.clone(), Cr.clone(), kr, system_id) if not rep0.zero_rhs \
-            else None
+        refreshed = (RecycleSpace(_own_colmajor(Ur), _own_colmajor(Cr), kr, system_id)
+                     if not rep0.zero_rhs else None)
     eng.c_cfg.flags = _lib.COLLECT_DIAGNOSTICS if collect_diagnostics else 0
     try:
         rep = eng.solve(dA, bt, x, x0t, U_ptr, ldu, k_in, stream=stream)
@@ -281,8 +281,11 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
         U, C, k, _ = eng.recycle_views()
         if k == 0:
             diag["gmres_fallback"] = True
-        out_space = RecycleSpace(U.t().contiguous().t() if k else U,
-                                 C.t().contiguous().t() if k else C, k, system_id)
+        # an independent copy (column-major): the RecycleSpace value must not
+        # alias the engine workspace, which the next solve overwrites (with
+        # ld == n a transposed .contiguous() would be a view)
+        out_space = RecycleSpace(_own_colmajor(U) if k else U, _own_colmajor(C) if k else C, k,
+                                 system_id)
     if collect_diagnostics:
         # gcrodr.py:372-376, :461-467, :484-485
         cap = cfg.max_iter + 2
@@ -311,6 +314,15 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
         x_device=x,
     )
     return report, out_space
+
+
+def _own_colmajor(X):
+    """Column-major copy of an (n, k) device view."""
+    import torch
+
+    out = torch.empty((X.shape[1], X.shape[0]), dtype=X.dtype, device=X.device)
+    out.copy_(X.t())
+    return out.t()
 
 
 def _recycle_residuals(dA: DeviceCsr, space: RecycleSpace):

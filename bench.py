@@ -530,6 +530,8 @@ def run_skr(args):
     value = n_sys_timed / (total_ms_max / 1000.0)
     its = [i for r in stats for i in r.iterations]
     conv_local = all(c for r in stats for c in r.converged)
+    unconv = [(int(i), int(it), float(tr)) for r in stats
+              for i, it, c, tr in zip(r.order, r.iterations, r.converged, r.true_rel) if not c]
     bytes_ = sum(r.spmv_ortho_bytes for r in stats)
     cyc_ms = sum(r.cycle_kernel_ms for r in stats)
     den_ms = sum(r.dense_kernel_ms for r in stats)
@@ -556,6 +558,8 @@ def run_skr(args):
         per_step_e, stats_e, _ = run_pass(host, "host")
         tot_e = all_max(sum(per_step_e))
         conv_e2e = all(c for r in stats_e for c in r.converged)
+        unconv += [(int(i), int(it), float(tr)) for r in stats_e
+                   for i, it, c, tr in zip(r.order, r.iterations, r.converged, r.true_rel) if not c]
         e2e = {"value": n_sys_timed / (tot_e / 1000.0), "unit": "systems/s",
                "h2d_bytes_per_step": int(sum(r.h2d_bytes for r in stats_e) / K),
                "d2h_bytes_per_step": int(sum(r.d2h_bytes for r in stats_e) / K),
@@ -615,6 +619,7 @@ def run_skr(args):
         "gpu_launches": int(launches),
         "clocks": clk,
         "iterations_mean": float(np.mean(its_all)), "all_converged": all_conv,
+        "unconverged_rank0": unconv[:16],
         "v0_projected_cycles": int(v0proj),
         "arnoldi_steps": int(steps_arn),
         "us_per_arnoldi_step": 1000.0 * cyc_ms / max(1, steps_arn),

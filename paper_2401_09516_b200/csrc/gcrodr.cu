@@ -692,11 +692,6 @@ constexpr double V0_PROJ_RTOL = 1e-12;
 
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
 constexpr int FUSE_COMB_ROWS = 4096;  // rows per CTA from which k_cycle applies the update
-#ifndef SKR_GM_STAGES
-#define SKR_GM_STAGES 2
-#endif
-constexpr int GM_STAGES = SKR_GM_STAGES;  // cp.async ring depth of the DMMA Gram pass
-constexpr int GM_MMAX = 40;  // Arnoldi length up to which the cycle end uses the DMMA Gram
 constexpr int GM_LD = 36;  // the same for the DMMA Gram (== 4 mod 16: conflict-free fragments)
 
 // k_cycle dynamic shared memory, sized by (m, kcap) (offsets in doubles):
@@ -715,10 +710,7 @@ __host__ __device__ inline int comb_ld(int m) {
 }
 inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
   CycleSmemLayout L;
-  // DMMA Gram ring (m <= GM_MMAX: GM_STAGES stages of kcap + m + 1 columns)
-  // or the CUDA-core Gram's single staging tile, + the x-update scratch
-  size_t gt = (m <= GM_MMAX ? (size_t)GM_STAGES * (kcap + m + 1) * GM_LD
-                            : (size_t)(2 * kcap + m + 1) * GT_LD) + NT;
+  size_t gt = (size_t)(2 * kcap + m + 1) * GM_LD + NT;  // + the x-update scratch
   if (gt < (size_t)NW * 2 * PVC) gt = (size_t)NW * 2 * PVC;
   // the cycle-start recycle update stages (2 kcap + m + 2) columns and then
   // the two coefficient blocks; at that point the R and B areas are free, so
@@ -1487,7 +1479,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   // dimension), in the same pass over the staged 32-row tiles as the x update
   // x += U (dk y1) + V y2, whose U and V columns are staged anyway; otherwise
   // the register-tiled CUDA-core Gram after the residual (below).
-  const bool gmma = defl && m <= GM_MMAX;
+  const bool gmma = defl && mm <= 40;
   auto tile_col = [&](int c) -> const double* {  // staged columns [U (kc) | C (kc) | V (j)]
     return (c < kc) ? colU(p, c) : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc)) : colV(p, c - 2 * kc);
   };
@@ -1517,41 +1509,35 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 #pragma unroll
       for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
     double* xpart = cdyn + p.sm_R - NT;  // last NT doubles of the Gram region
-    // the 32-row tiles stream through a GM_STAGES-deep shared-memory ring filled
-    // by 16-byte cp.async copies (L2 -> smem, no registers), GM_STAGES - 1
-    // tiles in flight while one is consumed; rows past r1 are zero-filled
-    const int gs = (kcap + m + 1) * GL;  // doubles per stage (ncs <= kcap + m + 1)
-    const int ntl = (r1 - r0 + 31) >> 5;
-    auto issue_tile = [&](int i) {
-      if (i < ntl) {
-        const int t0 = r0 + 32 * i;
-        double* dst = gtile + (i % GM_STAGES) * gs;
-        for (int e = tid; e < 16 * ncs; e += NT) {
-          const int c = e >> 4, rr = 2 * (e & 15), row = t0 + rr;
-          const int nbytes = row < r1 ? (row + 1 < r1 ? 16 : 8) : 0;
-          const double* src = tile_col(c) + (nbytes ? row : r0);
-          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + c * GL + rr);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
-                       "r"(nbytes) : "memory");
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
+    constexpr int GPF = 8;               // next tile's first elements, in flight
+    double pf[GPF];
+    auto load_tile = [&](int t0) {
 #pragma unroll
-    for (int i = 0; i < GM_STAGES - 1; ++i) issue_tile(i);
-    for (int it = 0; it < ntl; ++it) {
-      const int t0 = r0 + 32 * it;
-      asm volatile("cp.async.wait_group %0;" ::"n"(GM_STAGES - 2) : "memory");
-      __syncthreads();  // tile `it` landed for every thread; stage (it - 1) % GM_STAGES is free
-      issue_tile(it + GM_STAGES - 1);
-      const double* gtl = gtile + (it % GM_STAGES) * gs;
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT, row = t0 + (e & 31);
+        if (e < 32 * ncs) pf[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+      }
+    };
+    if (r0 < r1) load_tile(r0);
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+#pragma unroll
+      for (int k = 0; k < GPF; ++k) {
+        const int e = tid + k * NT;
+        if (e < 32 * ncs) gtile[(e >> 5) * GL + (e & 31)] = pf[k];
+      }
+      for (int e = tid + GPF * NT; e < 32 * ncs; e += NT) {
+        const int row = t0 + (e & 31);
+        gtile[(e >> 5) * GL + (e & 31)] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+      }
+      __syncthreads();
+      if (t0 + 32 < r1) load_tile(t0 + 32);
       // warp 0 fetches this tile's x now: its latency hides behind the DMMAs
       const double xold = (tid < 32 && t0 + tid < r1) ? p.x[t0 + tid] : 0.0;
       {  // x update partials: warp w sums the [U | V] columns c == w (mod NW)
         double xs = 0.0;
         for (int c = warp; c < kc + j; c += NW) {
           const int sc = c < kc ? c : 2 * kc + (c - kc);
-          xs = fma(gtl[sc * GL + lane], S.y[c], xs);
+          xs = fma(gtile[sc * GL + lane], S.y[c], xs);
         }
         xpart[warp * 32 + lane] = xs;
       }
@@ -1560,9 +1546,9 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         const int roff = 4 * (ks0 + kk);
         double af[3], bf[5];
 #pragma unroll
-        for (int x = 0; x < 3; ++x) af[x] = gtl[wa[x] + roff];
+        for (int x = 0; x < 3; ++x) af[x] = gtile[wa[x] + roff];
 #pragma unroll
-        for (int y = 0; y < 5; ++y) bf[y] = gtl[vb[y] + roff];
+        for (int y = 0; y < 5; ++y) bf[y] = gtile[vb[y] + roff];
 #pragma unroll
         for (int x = 0; x < 3; ++x)
           if (3 * h + x < nb)
@@ -1582,8 +1568,6 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         p.x[t0 + tid] = xold + xs;
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
     // the four k-step pairs of each half are added in warp order (fixed)
     double* gb = gtile;
     for (int q = 0; q < NW; ++q) {

@@ -34,7 +34,7 @@ from .sequence import (
     solve_sequence,
     split_chunks,
 )
-from .dataset import export_dataset
+from .dataset import DatasetWriter, export_dataset
 from .sorting import (
     ParameterMatrix,
     frobenius_distance,
@@ -52,7 +52,7 @@ __all__ = [
     "ChainState", "CsrMatrix", "DeviceCsr", "GcroDrEngine", "IdentityPreconditioner", "JacobiPreconditioner",
     "ParameterMatrix", "Preconditioner", "RecycleSpace", "SequenceResult", "SolveReport",
     "SolverConfig", "ZeroPivotError", "axpy", "build_preconditioner", "chunk_positions", "dot",
-    "eye", "export_dataset", "frobenius_distance", "gcrodr_solve", "gmres_solve", "greedy_sort",
+    "eye", "export_dataset", "DatasetWriter", "gather_results", "frobenius_distance", "gcrodr_solve", "gmres_solve", "greedy_sort",
     "greedy_sort_device", "grouped_sort", "grouped_sort_device", "harmonic_ritz_first_cycle", "harmonic_ritz_subsequent", "norm2",
     "sharded_greedy_sort", "chain_grid_ctas", "solve_chains", "solve_sequence", "split_chunks", "spmv",
 ]

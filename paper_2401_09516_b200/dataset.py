@@ -23,7 +23,7 @@ from .sparse import CsrMatrix
 from .sorting import ParameterMatrix
 
 __all__ = ["LinearSystem", "system_hash", "write_matrix_market", "write_vector",
-           "read_vector", "export_dataset"]
+           "read_vector", "export_dataset", "DatasetWriter"]
 
 
 @dataclass
@@ -118,3 +118,75 @@ def export_dataset(batch: Sequence[LinearSystem], reports: Optional[Sequence], o
     with open(path, "w") as fh:
         json.dump(manifest, fh, indent=2, sort_keys=True)
     return path
+
+
+class DatasetWriter:
+    """Streaming, multi-rank form of ``export_dataset``: every rank writes the
+    files of its own systems as their solves finish (``add``), so nothing but
+    the manifest rows is held; ``close`` gathers the manifest entries and the
+    parameter rows on rank 0 (object gather; NCCL or gloo), which writes
+    params.csv and manifest.json. For a batch whose ids are 0..n-1 the files
+    are byte-identical to ``export_dataset(batch, reports, out_dir, order,
+    config)`` in one process (tests/test_multirank_gloo.py). Single-process
+    use (no process group) works the same."""
+
+    def __init__(self, out_dir, order: Optional[Sequence[int]] = None, config=None, group=None):
+        self.out_dir = out_dir
+        self.order = None if order is None else [int(o) for o in order]
+        self.config = config
+        self.group = group
+        self.entries = []
+        self.params = []
+        os.makedirs(out_dir, exist_ok=True)
+
+    def add(self, system: LinearSystem, report=None) -> None:
+        stem = f"system_{system.id:04d}"
+        mtx, rhs = f"{stem}.mtx", f"{stem}_rhs.txt"
+        write_matrix_market(system.A, os.path.join(self.out_dir, mtx))
+        write_vector(system.b, os.path.join(self.out_dir, rhs))
+        entry = {"id": system.id, "problem_kind": system.problem_kind,
+                 "grid": list(system.grid), "matrix_file": mtx, "rhs_file": rhs,
+                 "matrix_hash": system_hash(system)}
+        if report is not None:
+            sol = f"{stem}_x.txt"
+            write_vector(report.x, os.path.join(self.out_dir, sol))
+            entry.update(solution_file=sol, iterations=report.iterations,
+                         converged=bool(report.converged),
+                         true_relative_residual=report.true_relative_residual,
+                         wall_time=report.wall_time)
+        self.entries.append(entry)
+        self.params.append((system.id, " ".join(_g17(system.params.flat))))
+
+    def close(self) -> Optional[str]:
+        entries, params = self.entries, self.params
+        try:
+            import torch.distributed as dist
+
+            dist_on = dist.is_available() and dist.is_initialized()
+        except ImportError:  # pragma: no cover
+            dist_on = False
+        if dist_on:
+            rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+            out = [None] * world if rank == 0 else None
+            dist.gather_object((entries, params), out, dst=0, group=self.group)
+            if rank != 0:
+                return None
+            entries = [e for part in out for e in part[0]]
+            params = [p for part in out for p in part[1]]
+        entries = sorted(entries, key=lambda e: e["id"])
+        params = sorted(params, key=lambda p: p[0])
+        with open(os.path.join(self.out_dir, "params.csv"), "w", newline="") as fh:
+            writer = csv.writer(fh)
+            writer.writerow(["system_id", "params"])
+            for sid, row in params:
+                writer.writerow([sid, row])
+        cfg = self.config
+        chash = cfg if cfg is None or isinstance(cfg, str) else cfg.config_hash()
+        n = len(entries)
+        manifest = {"n_systems": n,
+                    "solve_order": self.order if self.order is not None else list(range(n)),
+                    "config_hash": chash, "systems": entries}
+        path = os.path.join(self.out_dir, "manifest.json")
+        with open(path, "w") as fh:
+            json.dump(manifest, fh, indent=2, sort_keys=True)
+        return path

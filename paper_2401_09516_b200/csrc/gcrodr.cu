@@ -692,6 +692,7 @@ constexpr double V0_PROJ_RTOL = 1e-12;
 
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
 constexpr int FUSE_COMB_ROWS = 4096;  // rows per CTA from which k_cycle applies the update
+constexpr int GM_MMAX = 40;  // Arnoldi length up to which the cycle end uses the DMMA Gram
 constexpr int GM_LD = 36;  // the same for the DMMA Gram (== 4 mod 16: conflict-free fragments)
 
 // k_cycle dynamic shared memory, sized by (m, kcap) (offsets in doubles):
@@ -720,6 +721,15 @@ inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
   const size_t cmb_end = L.cmb + 2 * kb * (size_t)comb_ld(m);
   const size_t rb = (size_t)m * (m + 1) / 2 + (size_t)kcap * m;
   if (gt + rb < cmb_end) gt = cmb_end - rb;
+  // the cycle-end DMMA pass (m <= GM_MMAX) streams its tiles through two
+  // stages [0, gs) and [gs + NT, 2 gs + NT) around the x-update scratch; the
+  // second stage may run into R and B (dead at the cycle end), so at C3 the
+  // ring fits in the footprint the cycle-start update needs anyway (shared
+  // memory, and with it L1 -- which sweep 2 depends on -- is unchanged)
+  if (m <= GM_MMAX) {
+    const size_t gs = (size_t)(kcap + m + 1) * GM_LD;
+    if (gt + rb < 2 * gs + NT) gt = 2 * gs + NT - rb;
+  }
   L.R = gt;
   L.B = L.R + (size_t)m * (m + 1) / 2;
   L.csr = (L.B + (size_t)kcap * m + 1) & ~(size_t)1;  // 16-byte aligned
@@ -1479,7 +1489,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   // dimension), in the same pass over the staged 32-row tiles as the x update
   // x += U (dk y1) + V y2, whose U and V columns are staged anyway; otherwise
   // the register-tiled CUDA-core Gram after the residual (below).
-  const bool gmma = defl && mm <= 40;
+  const bool gmma = defl && m <= GM_MMAX;
   auto tile_col = [&](int c) -> const double* {  // staged columns [U (kc) | C (kc) | V (j)]
     return (c < kc) ? colU(p, c) : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc)) : colV(p, c - 2 * kc);
   };
@@ -1508,36 +1518,42 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     for (int x = 0; x < 3; ++x)
 #pragma unroll
       for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-    double* xpart = cdyn + p.sm_R - NT;  // last NT doubles of the Gram region
-    constexpr int GPF = 8;               // next tile's first elements, in flight
-    double pf[GPF];
-    auto load_tile = [&](int t0) {
-#pragma unroll
-      for (int k = 0; k < GPF; ++k) {
-        const int e = tid + k * NT, row = t0 + (e & 31);
-        if (e < 32 * ncs) pf[k] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
+    // tiles through a two-stage shared-memory ring filled by 16-byte cp.async
+    // copies (no registers: the pass's DMMA accumulators need them), one
+    // tile in flight while the other is consumed; rows past r1 zero-filled
+    const int gs = (kcap + m + 1) * GL;  // doubles per stage (ncs <= kcap + m + 1)
+    double* xpart = cdyn + gs;           // x-update scratch between the stages
+    double* stage1 = cdyn + gs + NT;
+    const int ntl = (r1 - r0 + 31) >> 5;
+    auto issue_tile = [&](int i) {
+      if (i < ntl) {
+        const int t0 = r0 + 32 * i;
+        double* dst = (i & 1) ? stage1 : gtile;
+        for (int e = tid; e < 16 * ncs; e += NT) {
+          const int c = e >> 4, rr = 2 * (e & 15), row = t0 + rr;
+          const int nbytes = row < r1 ? (row + 1 < r1 ? 16 : 8) : 0;
+          const double* src = tile_col(c) + (nbytes ? row : r0);
+          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + c * GL + rr);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+                       "r"(nbytes) : "memory");
+        }
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (r0 < r1) load_tile(r0);
-    for (int t0 = r0; t0 < r1; t0 += 32) {
-#pragma unroll
-      for (int k = 0; k < GPF; ++k) {
-        const int e = tid + k * NT;
-        if (e < 32 * ncs) gtile[(e >> 5) * GL + (e & 31)] = pf[k];
-      }
-      for (int e = tid + GPF * NT; e < 32 * ncs; e += NT) {
-        const int row = t0 + (e & 31);
-        gtile[(e >> 5) * GL + (e & 31)] = row < r1 ? tile_col(e >> 5)[row] : 0.0;
-      }
-      __syncthreads();
-      if (t0 + 32 < r1) load_tile(t0 + 32);
+    issue_tile(0);
+    for (int it = 0; it < ntl; ++it) {
+      const int t0 = r0 + 32 * it;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();  // tile `it` landed for every thread; the other stage is consumed
+      issue_tile(it + 1);
+      const double* gtl = (it & 1) ? stage1 : gtile;
       // warp 0 fetches this tile's x now: its latency hides behind the DMMAs
       const double xold = (tid < 32 && t0 + tid < r1) ? p.x[t0 + tid] : 0.0;
       {  // x update partials: warp w sums the [U | V] columns c == w (mod NW)
         double xs = 0.0;
         for (int c = warp; c < kc + j; c += NW) {
           const int sc = c < kc ? c : 2 * kc + (c - kc);
-          xs = fma(gtile[sc * GL + lane], S.y[c], xs);
+          xs = fma(gtl[sc * GL + lane], S.y[c], xs);
         }
         xpart[warp * 32 + lane] = xs;
       }
@@ -1546,9 +1562,9 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         const int roff = 4 * (ks0 + kk);
         double af[3], bf[5];
 #pragma unroll
-        for (int x = 0; x < 3; ++x) af[x] = gtile[wa[x] + roff];
+        for (int x = 0; x < 3; ++x) af[x] = gtl[wa[x] + roff];
 #pragma unroll
-        for (int y = 0; y < 5; ++y) bf[y] = gtile[vb[y] + roff];
+        for (int y = 0; y < 5; ++y) bf[y] = gtl[vb[y] + roff];
 #pragma unroll
         for (int x = 0; x < 3; ++x)
           if (3 * h + x < nb)
@@ -1568,6 +1584,8 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         p.x[t0 + tid] = xold + xs;
       }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
     // the four k-step pairs of each half are added in warp order (fixed)
     double* gb = gtile;
     for (int q = 0; q < NW; ++q) {

@@ -75,6 +75,9 @@ def _args():
                     help="CTAs of each chain's Arnoldi kernel (default: chain_grid_ctas)")
     ap.add_argument("--n-systems", type=int, default=None, help="override batch size")
     ap.add_argument("--grid", type=int, default=None, help="override grid side (testing)")
+    ap.add_argument("--gen", default="host", choices=["host", "device"],
+                    help="parameter generator: host numpy (the inputs the reference goldens "
+                         "pin) or the device Philox generator (csrc/grf.cu)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sync-steps", action="store_true",
@@ -380,14 +383,21 @@ def run_skr(args):
     NC = max(1, args.chains)
     if S % NC:
         raise SystemExit(f"--stripe {S} must be a multiple of --chains {NC}")
+    sub = S // NC  # systems per chain per step
     gctas = skr.chain_grid_ctas(NC) if args.ctas_per_chain is None else args.ctas_per_chain
     cfg = skr.SolverConfig(m=spec.m, tol=spec.tol, max_iter=spec.max_iter, k=spec.k)
     jac = spec.precond == "jacobi"
     # ---- parameters + sort (sharded rows + all_gather when world > 1) -------
     t_gen = time.perf_counter()
-    flat = _params(spec)
+    if args.gen == "device":  # sampled in place on the GPU (no host copy)
+        flat_d, gen_extra = P.params_device(spec)
+        torch.cuda.synchronize()
+        flat = None
+    else:
+        flat = _params(spec)
     gen_s = time.perf_counter() - t_gen
-    flat_d = torch.from_numpy(flat).to(dev)
+    if flat is not None:
+        flat_d = torch.from_numpy(flat).to(dev)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -395,7 +405,8 @@ def run_skr(args):
     e1.record()
     torch.cuda.synchronize()
     sort_ms = e0.elapsed_time(e1)
-    del flat_d
+    if flat is not None:
+        del flat_d
     # ---- this rank's chunk of the chain ------------------------------------
     chunk = list(skr.chunk_positions(spec.n_systems, world, rank))
     need = (W + K) * S
@@ -412,14 +423,19 @@ def run_skr(args):
     # stencil form assembled on the GPU (bit-identical to the host assembly)
     dev_sys = []
     for i in idxs:
-        dA, b, _ = P.assemble_device(spec, i, _fields(spec, i, flat), jacobi=jac)
+        f = (_fields(spec, i, flat) if flat is not None else
+             P.fields_from_params_device(spec, flat_d[i], gen_extra[i]))
+        dA, b, _ = P.assemble_device(spec, i, f, jacobi=jac)
         dev_sys.append((dA, b))
     torch.cuda.synchronize()
-    n_params = int(flat.shape[1])
+    n_params = int((flat if flat is not None else flat_d).shape[1])
     # the CPU baseline's sample needs a few systems' fields; the rest of the
     # parameters (C3: 8.6 GB per rank) are released
-    cpu_rows = {i: flat[i].copy() for i in idxs[W * sub: W * sub + 4]}
+    cpu_rows = {i: (flat[i].copy() if flat is not None else flat_d[i].cpu().numpy())
+                for i in idxs[W * sub: W * sub + 4]}
     del flat
+    if args.gen == "device":
+        del flat_d  # the assembled systems keep their own coefficient fields
     # pinned host copies of the same systems for the end-to-end pass (the
     # sparsity pattern is one pinned array pair; its bytes are still uploaded
     # for every system)
@@ -438,7 +454,6 @@ def run_skr(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    sub = S // NC          # systems per chain per step
     span = (W + K) * sub   # positions per chain (contiguous sub-chunk of this rank's chunk)
     # pinned host buffer for the e2e read-back of x: one row per position
     x_pinned = (torch.empty((need, spec.N), dtype=torch.float64, pin_memory=True)
@@ -596,7 +611,7 @@ def run_skr(args):
         "warmup": W, "ms_per_step": total_ms_max / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator; DCT-sampled GRF, see DESIGN.md)",
-        "config": dict(_config_dict(spec, S, world, NC), chunk_wrapped=wrapped,
+        "config": dict(_config_dict(spec, S, world, NC), generator=args.gen, chunk_wrapped=wrapped,
                        distinct_systems=distinct, ctas_per_chain=gctas,
                        l2=("flushed between steps (256 MiB write)" if args.sync_steps else
                            "flushed (256 MiB write) before the timed region; inside it every "

@@ -648,7 +648,7 @@ def run_skr(args):
                           "chain_wall_ms": sorted(round(1000 * r.wall_s, 1) for r in stats),
                           "total": total_ms},
         "sort": {"ms": sort_ms, "n_systems": spec.n_systems, "P": n_params,
-                 "param_generation_s": round(gen_s, 1)},
+                 "param_generation_s": round(gen_s, 3)},
     }
     if cpu is not None:
         out["cpu_baseline"] = cpu

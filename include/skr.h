@@ -145,6 +145,28 @@ int skr_assemble_fd(int32_t kind, int32_t dim, int32_t n, const double* field, d
                     const int32_t* row_ptr, double* values, void* stencil, size_t stencil_bytes,
                     void* stream);
 
+/* Device sampling of the configs' coefficient fields (the
+ * device counterpart of problems.system_params, which stands in for the
+ * reference's samplers kryrec/problems.py:97-162 seeded per system as :488).
+ * White noise = Philox4x32-10 (key = (seed_lo, seed_hi ^ cid), counter =
+ * (pair_lo, pair_hi, idx, stream)) + Box-Muller; stream 0 of system idx is the
+ * field's noise. g = DCT-III_ortho along every axis of xi * coef,
+ * coef = 1 / (pi^2 |kappa|^2 + tau^2) (coef_0 = 0), divided by norm; then
+ * kind 0: field = g > 0 ? 12 : 3; kind 1: exp(param g); kind 2: param (1 +
+ * 0.3 tanh g). dct = [T | T^T], T the n x n orthonormal DCT-III matrix
+ * (T[k][j] = c_j cos(pi j (2k + 1) / (2n))). g_out (optional) receives g.
+ * Stream-ordered, allocates nothing (work >= skr_grf_workspace_bytes). */
+size_t skr_grf_workspace_bytes(int32_t dim, int32_t n);
+int skr_grf_sample(int32_t dim, int32_t n, int32_t kind, double tau, double param, double norm,
+                   const double* dct, uint64_t seed, uint32_t cid, uint32_t idx, double* field,
+                   double* g_out, void* work, size_t work_bytes, void* stream);
+/* count N(0,1) samples (times scale) / [0,1) uniforms of (system idx, stream)
+ * of the same generator (the C1 right-hand side noise, C2's k0 and centre). */
+int skr_philox_normals(int64_t count, uint64_t seed, uint32_t cid, uint32_t idx,
+                       uint32_t stream_id, double scale, double* out, void* stream);
+int skr_philox_uniforms(int32_t count, uint64_t seed, uint32_t cid, uint32_t idx,
+                        uint32_t stream_id, double* out, void* stream);
+
 size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter);
 /* Solve A x = b with GCRO-DR. U_in (n x k_in, column-major, leading dim ldu)
  * is the previous system's recycle U (its C is not needed: the refresh

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("SKR_LIB_PATH") or os.path.join(PKG, "libskr.so")
 EXPORTS = (
     "skr_version", "skr_status_string", "skr_device_info", "skr_spmv", "skr_residual",
     "skr_stencil_bytes", "skr_stencil_build", "skr_assemble_fd",
+    "skr_grf_workspace_bytes", "skr_grf_sample", "skr_philox_normals", "skr_philox_uniforms",
     "skr_gcrodr_workspace_bytes", "skr_gcrodr_solve", "skr_gcrodr_recycle_view",
     "skr_gcrodr_profile", "skr_gcrodr_solve_chains", "skr_gcrodr_diagnostics",
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
@@ -82,6 +83,14 @@ def _declare(L):
         "skr_assemble_fd": ([c_int32, c_int32, c_int32, P, c_double, P, P, P, ctypes.c_size_t, P],
                             c_int32),
         "skr_residual": ([POINTER(SkrCsr), P, P, P, c_int32, P], c_int32),
+        "skr_grf_workspace_bytes": ([c_int32, c_int32], c_size_t),
+        "skr_grf_sample": ([c_int32, c_int32, c_int32, c_double, c_double, c_double, P,
+                            ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, P, P, P, c_size_t,
+                            P], c_int32),
+        "skr_philox_normals": ([c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                ctypes.c_uint32, c_double, P, P], c_int32),
+        "skr_philox_uniforms": ([c_int32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                 ctypes.c_uint32, P, P], c_int32),
         "skr_gcrodr_workspace_bytes": ([c_int32, c_int32, c_int32, c_int32], c_size_t),
         "skr_gcrodr_solve": ([POINTER(SkrCsr), P, P, P, POINTER(SkrConfig), P, c_int32, c_int32,
                               P, c_size_t, POINTER(SkrReport), P, c_int32, P, c_int32, P],

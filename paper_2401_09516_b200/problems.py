@@ -42,6 +42,11 @@ __all__ = [
     "assemble_device",
     "rhs",
     "csr_pattern",
+    "dct_matrix",
+    "system_params_device",
+    "params_device",
+    "fields_from_params_device",
+    "rhs_device",
 ]
 
 BASE_SEED = 240109516
@@ -229,6 +234,154 @@ def rhs(spec: ConfigSpec, fields: dict) -> np.ndarray:
     raise ValueError(spec.kind)
 
 
+# ---------------------------------------------------------------------------
+# device generator ("philox" inputs, csrc/grf.cu)
+# ---------------------------------------------------------------------------
+_KIND_CODE = {"darcy_binary": 0, "poisson_lognormal": 1, "helmholtz": 2}
+_DCT_DEV: dict = {}
+
+
+@lru_cache(maxsize=8)
+def dct_matrix(n: int) -> np.ndarray:
+    """Orthonormal DCT-III matrix T (T @ v == scipy idct(v, type=2, norm="ortho"))."""
+    j = np.arange(n)
+    T = np.cos(np.pi * np.outer(2 * j + 1, j) / (2.0 * n))
+    T[:, 0] *= np.sqrt(1.0 / n)
+    T[:, 1:] *= np.sqrt(2.0 / n)
+    return T
+
+
+def _dct_device(n: int, dev):
+    key = (n, dev.index)
+    if key not in _DCT_DEV:
+        import torch
+
+        T = dct_matrix(n)
+        _DCT_DEV[key] = torch.from_numpy(np.concatenate([T.ravel(), T.T.copy().ravel()])).to(dev)
+    return _DCT_DEV[key]
+
+
+def _grf_work(spec: ConfigSpec, dev):
+    import torch
+
+    from . import _lib
+
+    nb = int(_lib.load().skr_grf_workspace_bytes(spec.dim, spec.n))
+    return torch.empty(nb // 8, dtype=torch.float64, device=dev)
+
+
+def system_params_device(spec: ConfigSpec, idx: int, stream=None, out=None, work=None,
+                         seed: int = BASE_SEED) -> dict:
+    """The coefficient field of system ``idx`` sampled on the GPU
+    (``skr_grf_sample``): Philox4x32-10 white noise, the DCT spectrum of
+    ``grf`` and the coefficient laws of ``system_params``, nothing on the
+    host. A seeded generator of its own (the host ``system_params`` draws from
+    numpy's PCG64): same distribution, different samples. ``out`` (optional,
+    a device row of length P) receives the sort parameters in place, so a
+    whole batch can be written straight into the parameter matrix. Returns
+    device tensors ``a`` / ``kfield`` (+ ``g``), ``params`` and, for
+    Helmholtz, the host scalars ``k0`` and ``center``."""
+    import torch
+
+    from . import _lib
+
+    _lib.require_cuda()
+    L = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dim, n = spec.dim, spec.n
+    N = n ** dim
+    kind = _KIND_CODE[spec.kind]
+    P = N + 1 if kind == 2 else N
+    params = out if out is not None else torch.empty(P, dtype=torch.float64, device=dev)
+    if params.numel() != P or params.dtype != torch.float64 or not params.is_contiguous():
+        raise ValueError(f"out must be a contiguous float64 device vector of length {P}")
+    work = work if work is not None else _grf_work(spec, dev)
+    ctx = torch.cuda.stream(stream) if stream is not None else _null()
+    _, norm = _spectrum((n,) * dim, float(spec.tau))
+    res: dict = {}
+    with ctx:
+        sh = _lib.stream_handle(stream)
+        if kind == 2:
+            u = torch.empty(1 + dim, dtype=torch.float64, device=dev)
+            _lib.check(L.skr_philox_uniforms(1 + dim, seed, spec.cid, idx, 1, u.data_ptr(), sh),
+                       "skr_philox_uniforms")
+            uh = u.cpu().numpy()
+            k0 = 10.0 + 10.0 * float(uh[0])
+            field = torch.empty(N, dtype=torch.float64, device=dev)
+            g = params[1:]
+            params[0] = k0
+            res.update(k0=k0, center=0.2 + 0.6 * uh[1:1 + dim], kfield=field.view((n,) * dim),
+                       g=g.view((n,) * dim))
+            param, gp = k0, g.data_ptr()
+        else:
+            field, gp = params, 0
+            param = spec.scale
+            res["a"] = field.view((n,) * dim)
+        _lib.check(L.skr_grf_sample(dim, n, kind, float(spec.tau), float(param), float(norm),
+                                    _dct_device(n, dev).data_ptr(), seed, spec.cid, idx,
+                                    field.data_ptr(), gp, work.data_ptr(), work.numel() * 8, sh),
+                   "skr_grf_sample")
+    res["params"] = params
+    return res
+
+
+def params_device(spec: ConfigSpec, idxs=None, stream=None, seed: int = BASE_SEED):
+    """(n_systems x P) device parameter matrix of the device generator (the
+    sort's input), every row sampled in place; one workspace, one stream."""
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    idxs = list(range(spec.n_systems)) if idxs is None else list(idxs)
+    P = spec.N + 1 if spec.kind == "helmholtz" else spec.N
+    flat = torch.empty((len(idxs), P), dtype=torch.float64, device=dev)
+    work = _grf_work(spec, dev)
+    extra = []
+    for r, i in enumerate(idxs):
+        f = system_params_device(spec, i, stream=stream, out=flat[r], work=work, seed=seed)
+        extra.append({k: f[k] for k in ("k0", "center") if k in f})
+    return flat, extra
+
+
+def fields_from_params_device(spec: ConfigSpec, row, extra: dict | None = None) -> dict:
+    """Device fields of one system from its device parameter row (the inverse
+    of ``params``): a = row (Darcy / Poisson); Helmholtz k = k0 (1 + 0.3 tanh g)
+    recomputed from g = row[1:] (the elementwise law, torch plumbing)."""
+    import torch
+
+    n, dim = spec.n, spec.dim
+    if spec.kind != "helmholtz":
+        return {"a": row.view((n,) * dim), "params": row}
+    k0 = float(extra["k0"])
+    g = row[1:]
+    kf = k0 * (1.0 + 0.3 * torch.tanh(g))
+    return {"kfield": kf.view((n,) * dim), "k0": k0, "g": g.view((n,) * dim),
+            "center": extra["center"], "params": row}
+
+
+def rhs_device(spec: ConfigSpec, fields: dict, stream=None, seed: int = BASE_SEED):
+    """b on the device for the device generator: Darcy -h^2, Poisson -h^2 f with
+    f the generator's (system 0, stream 7) normals, Helmholtz the host bump
+    (N doubles) uploaded."""
+    import torch
+
+    from . import _lib
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    N = spec.N
+    h = 1.0 / (spec.n + 1)
+    if spec.kind == "darcy_binary":
+        return torch.full((N,), -(h * h), dtype=torch.float64, device=dev)
+    if spec.kind == "poisson_lognormal":
+        b = torch.empty(N, dtype=torch.float64, device=dev)
+        ctx = torch.cuda.stream(stream) if stream is not None else _null()
+        with ctx:
+            _lib.check(_lib.load().skr_philox_normals(N, seed, spec.cid, 0, 7, -(h * h),
+                                                      b.data_ptr(), _lib.stream_handle(stream)),
+                       "skr_philox_normals")
+        return b
+    return torch.from_numpy(rhs(spec, fields)).to(dev)
+
+
 _PATTERN_DEV: dict = {}
 
 
@@ -260,8 +413,11 @@ def assemble_device(spec: ConfigSpec, idx: int, fields: dict | None = None, stre
     field = fields["kfield"] if kind else fields["a"]
     ctx = torch.cuda.stream(stream) if stream is not None else _null()
     with ctx:
-        f_d = torch.from_numpy(np.ascontiguousarray(field, dtype=np.float64).ravel()).to(
-            dev, non_blocking=True)
+        if isinstance(field, torch.Tensor):  # device generator output
+            f_d = field.reshape(-1)
+        else:
+            f_d = torch.from_numpy(np.ascontiguousarray(field, dtype=np.float64).ravel()).to(
+                dev, non_blocking=True)
         vals = torch.empty(ci_d.numel(), dtype=torch.float64, device=dev)
         sx, sxy = n, (n * n if dim == 3 else 0)
         nbytes = int(L.skr_stencil_bytes(N, sx, sxy))
@@ -269,7 +425,10 @@ def assemble_device(spec: ConfigSpec, idx: int, fields: dict | None = None, stre
         _lib.check(L.skr_assemble_fd(kind, dim, n, f_d.data_ptr(), h, rp_d.data_ptr(),
                                      vals.data_ptr(), buf.data_ptr(), nbytes,
                                      _lib.stream_handle(stream)), "skr_assemble_fd")
-        b_d = torch.from_numpy(rhs(spec, fields)).to(dev, non_blocking=True)
+        if isinstance(field, torch.Tensor):
+            b_d = rhs_device(spec, fields, stream=stream)
+        else:
+            b_d = torch.from_numpy(rhs(spec, fields)).to(dev, non_blocking=True)
         jac = (spec.precond == "jacobi") if jacobi is None else jacobi
         # Jacobi diagonal = the stencil form's D (strictly negative for the flux
         # operators: minus a sum of positive face coefficients)

@@ -18,6 +18,10 @@
  *   skr_sort_chain      <- sorting.greedy_sort / _greedy_chain (sorting.py:55-80)
  *   skr_dense_hr_first  <- gcrodr.harmonic_ritz_first_cycle (gcrodr.py:173-206)
  *   skr_dense_hr_next   <- gcrodr.harmonic_ritz_subsequent (gcrodr.py:209-240)
+ *   skr_precond_build /
+ *   skr_precond_apply   <- precond.build_preconditioner (precond.py:251-312) and
+ *                          the SOR / ILU(0) / IC(0) / block-Jacobi apply
+ *                          (precond.py:80-145)
  */
 #ifndef SKR_H_
 #define SKR_H_
@@ -55,6 +59,11 @@ typedef struct skr_csr {
   const void* stencil;
   int32_t sx;
   int32_t sxy;
+  /* Optional general left preconditioner (NULL = none): a device buffer built
+   * by skr_precond_build from this matrix (SOR, ILU(0), IC(0), block Jacobi).
+   * When set it replaces diag: every op(v) = M^-1 (A v) and every
+   * preconditioned residual solves M z = v with the stored factorization. */
+  const void* precond;
 } skr_csr;
 
 /* SolverConfig (gmres.py:26-43) + one launch knob. */
@@ -166,6 +175,25 @@ int skr_philox_normals(int64_t count, uint64_t seed, uint32_t cid, uint32_t idx,
                        uint32_t stream_id, double scale, double* out, void* stream);
 int skr_philox_uniforms(int32_t count, uint64_t seed, uint32_t cid, uint32_t idx,
                         uint32_t stream_id, double* out, void* stream);
+
+/* General left preconditioners (kryrec/precond.py:80-145 SOR / ILU(0) / IC(0) /
+ * block Jacobi classes, :161-248 the factorizations, :251-312
+ * build_preconditioner). skr_precond_build analyses and factors A on the device
+ * into buf (>= skr_precond_bytes): dependency levels of the triangular sweeps,
+ * the ILU(0) / IC(0) factor on A's own pattern in the reference's operation
+ * order (IC(0) on -A when every diagonal entry is negative), M = D / omega + L
+ * for SOR, per-block dense LU with partial pivoting (block <= 256) for block
+ * Jacobi. A's row_ptr / col_idx (sorted rows) must outlive buf. info (host, may
+ * be NULL: then the call does not synchronise) receives [0] = 0 ok, 1 zero (IC:
+ * nonpositive) pivot = ZeroPivotError(kind, row = info[1], *value), 2 matrix not
+ * symmetric (IC(0) only; ValueError in the reference). skr_precond_apply solves
+ * M z = v for ncols columns (in == out allowed); one apply per buffer at a time. */
+enum skr_precond_kind { SKR_PC_SOR = 1, SKR_PC_ILU0 = 2, SKR_PC_ICC0 = 3, SKR_PC_BJACOBI = 4 };
+size_t skr_precond_bytes(int32_t kind, int32_t n, int32_t nnz, int32_t block);
+int skr_precond_build(const skr_csr* A, int32_t kind, double omega, int32_t block, void* buf,
+                      size_t bytes, int32_t* info, double* value, void* stream);
+int skr_precond_apply(const void* precond, const double* in, double* out, int32_t ncols,
+                      int64_t ld_in, int64_t ld_out, void* stream);
 
 size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter);
 /* Solve A x = b with GCRO-DR. U_in (n x k_in, column-major, leading dim ldu)

@@ -166,27 +166,185 @@ def reference_distance(p: np.ndarray, q: np.ndarray) -> float:
 # operator (sparse.py:76-83, gmres.py:184-190, precond.py:59-77)
 # --------------------------------------------------------------------------
 class Operator:
-    """op(v) = M^{-1}(A v) with M = I or diag(A); blocks act column-wise."""
+    """op(v) = M^{-1}(A v) with M = I, diag(A) or a general preconditioner
+    (``prec``: a ``GeneralPrec``); blocks act column-wise."""
 
-    def __init__(self, row_ptr, col_idx, values, n, jacobi: bool):
+    def __init__(self, row_ptr, col_idx, values, n, jacobi: bool, prec=None):
         self.n = int(n)
         self.S = sp.csr_matrix(
             (np.asarray(values, np.float64), np.asarray(col_idx, np.int64),
              np.asarray(row_ptr, np.int64)), shape=(self.n, self.n))
         self.diag = self.S.diagonal() if jacobi else None
+        self.general = prec
         if self.diag is not None and np.any(self.diag == 0.0):
             raise ValueError("jacobi: zero pivot")  # precond.py:153-158
 
     def prec(self, v):
         v = np.asarray(v, dtype=np.float64)
+        if self.general is not None:
+            return self.general.apply(v)
         if self.diag is None:
             return np.array(v, dtype=np.float64, copy=True)
         return v / (self.diag if v.ndim == 1 else self.diag[:, None])
 
     def __call__(self, v):
-        if self.diag is None:
+        if self.diag is None and self.general is None:
             return self.S @ v
         return self.prec(self.S @ v)
+
+
+# --------------------------------------------------------------------------
+# general preconditioners (precond.py:80-145, :161-312)
+# --------------------------------------------------------------------------
+class ZeroPivot(ValueError):
+    def __init__(self, kind, row, value=0.0):
+        self.kind, self.row, self.value = kind, int(row), float(value)
+        super().__init__(f"{kind}: zero pivot at row {self.row} (value {value:g})")
+
+
+def ilu0_values(row_ptr, col_idx, values):
+    """IKJ ILU(0) on A's own pattern (precond.py:170-216): the factor as values
+    on the pattern (multipliers l_ik left of the diagonal, U from it on). The
+    same scalar operations in the same order as the reference's loops."""
+    ptr = np.asarray(row_ptr, np.int64)
+    col = np.asarray(col_idx, np.int64)
+    val = np.array(values, dtype=np.float64)
+    n = len(ptr) - 1
+    pos = [{int(c): q for q, c in enumerate(col[ptr[i]:ptr[i + 1]], start=int(ptr[i]))}
+           for i in range(n)]
+    dpos = np.empty(n, dtype=np.int64)
+    for i in range(n):
+        q = pos[i].get(i, -1)
+        if q < 0 or val[q] == 0.0:
+            raise ZeroPivot("ilu0", i)
+        dpos[i] = q
+    for i in range(n):
+        lo, hi = int(ptr[i]), int(ptr[i + 1])
+        for p in range(lo, hi):
+            k = int(col[p])
+            if k >= i:
+                break
+            pivot = val[dpos[k]]
+            if pivot == 0.0:
+                raise ZeroPivot("ilu0", k)
+            lik = val[p] / pivot
+            val[p] = lik
+            rk = pos[k]
+            for q in range(p + 1, hi):
+                pk = rk.get(int(col[q]))
+                if pk is not None:
+                    val[q] -= lik * val[pk]
+    for i in range(n):
+        if val[dpos[i]] == 0.0:
+            raise ZeroPivot("ilu0", i)
+    return val, dpos
+
+
+def icc0_values(row_ptr, col_idx, values, sign):
+    """IC(0) of sign * A on the lower triangle of A's pattern
+    (precond.py:219-248): L as values on the pattern positions j <= i."""
+    ptr = np.asarray(row_ptr, np.int64)
+    col = np.asarray(col_idx, np.int64)
+    aval = np.asarray(values, np.float64)
+    n = len(ptr) - 1
+    rows = [dict() for _ in range(n)]
+    out = np.zeros(len(aval))
+    for i in range(n):
+        li = rows[i]
+        for p in range(int(ptr[i]), int(ptr[i + 1])):
+            j = int(col[p])
+            if j > i:
+                break
+            a_ij = sign * aval[p]
+            if j < i:
+                lj = rows[j]
+                s = a_ij
+                for k, lik in li.items():
+                    ljk = lj.get(k)
+                    if ljk is not None:
+                        s -= lik * ljk
+                li[j] = s / lj[j]
+                out[p] = li[j]
+            else:
+                d = a_ij - sum(x * x for k, x in li.items() if k < i)
+                if d <= 0.0:
+                    raise ZeroPivot("icc0", i, d)
+                li[i] = float(np.sqrt(d))
+                out[p] = li[i]
+    return out
+
+
+class GeneralPrec:
+    """solve M z = v for M of kind sor | ilu0 | icc0 | bjacobi
+    (precond.py:80-145). The reference hands the triangular factors to
+    non-pivoting SuperLU; here they are solved by scipy's substitution, which
+    agrees with it to rounding (pinned at 1e-12 by tests/golden/precond.npz)."""
+
+    def __init__(self, row_ptr, col_idx, values, n, kind, sor_omega=1.0, bjacobi_block=64):
+        import scipy.sparse.linalg as spla
+
+        self.kind = kind
+        self.n = int(n)
+        S = sp.csr_matrix((np.asarray(values, np.float64), np.asarray(col_idx, np.int64),
+                           np.asarray(row_ptr, np.int64)), shape=(n, n))
+        rows = np.repeat(np.arange(n), np.diff(np.asarray(row_ptr, np.int64)))
+        col = np.asarray(col_idx, np.int64)
+        tri = lambda M, lower: (lambda v: spla.spsolve_triangular(  # noqa: E731
+            sp.csr_matrix(M), v, lower=lower))
+        if kind == "sor":  # precond.py:285-292
+            diag = S.diagonal()
+            if np.any(diag == 0.0):
+                raise ZeroPivot("sor", np.flatnonzero(diag == 0.0)[0])
+            M = sp.tril(S, k=-1, format="csr") + sp.diags(diag / float(sor_omega), format="csr")
+            self._steps = [tri(M, True)]
+            self.scale = 1.0
+        elif kind == "ilu0":  # precond.py:294-297
+            fv, _ = ilu0_values(row_ptr, col_idx, values)
+            self.factor = fv
+            lo = col < rows
+            Lm = sp.csr_matrix((fv[lo], (rows[lo], col[lo])), shape=(n, n)) + sp.identity(n)
+            Um = sp.csr_matrix((fv[~lo], (rows[~lo], col[~lo])), shape=(n, n))
+            self._steps = [tri(Lm, True), tri(Um, False)]
+            self.scale = 1.0
+        elif kind == "icc0":  # precond.py:299-306
+            if abs(S - S.T).nnz != 0:
+                raise ValueError("icc0 requires a symmetric matrix (pattern and values)")
+            diag = S.diagonal()
+            if np.any(diag == 0.0):
+                raise ZeroPivot("icc0", np.flatnonzero(diag == 0.0)[0])
+            self.scale = -1.0 if np.all(diag < 0.0) else 1.0
+            fv = icc0_values(row_ptr, col_idx, values, self.scale)
+            self.factor = fv
+            lo = col <= rows
+            Lm = sp.csr_matrix((fv[lo], (rows[lo], col[lo])), shape=(n, n))
+            self._steps = [tri(Lm, True), tri(sp.csr_matrix(Lm.T), False)]
+        elif kind == "bjacobi":  # precond.py:270-283
+            bs = int(bjacobi_block)
+            fac = []
+            for start in range(0, n, bs):
+                end = min(n, start + bs)
+                lu, piv = sla.lu_factor(S[start:end, start:end].toarray(), check_finite=False)
+                bad = np.flatnonzero(np.diag(lu) == 0.0)
+                if len(bad):
+                    raise ZeroPivot("bjacobi", start + bad[0])
+                fac.append((start, end, lu, piv))
+
+            def blocks(v):
+                z = np.empty_like(v)
+                for start, end, lu, piv in fac:
+                    z[start:end] = sla.lu_solve((lu, piv), v[start:end])
+                return z
+
+            self._steps = [blocks]
+            self.scale = 1.0
+        else:
+            raise ValueError(f"unknown preconditioner kind {kind!r}")
+
+    def apply(self, v):
+        z = np.asarray(v, dtype=np.float64)
+        for f in self._steps:
+            z = f(z)
+        return self.scale * z if self.scale != 1.0 else z
 
 
 # --------------------------------------------------------------------------

@@ -3,7 +3,7 @@
 Drop-in surface of the reference package ``kryrec`` for the hot path
 (kryrec/__init__.py): ``greedy_sort``, ``gcrodr_solve``, ``SolverConfig``,
 ``SolveReport``, ``RecycleSpace``, ``build_preconditioner`` ('none' |
-'jacobi'), ``CsrMatrix`` -- plus ``solve_sequence`` (the chained solve of
+'jacobi' | 'bjacobi' | 'sor' | 'ilu0' | 'icc0'), ``CsrMatrix`` -- plus ``solve_sequence`` (the chained solve of
 harness.py:233-260 with the recycle pair resident on the GPU) and
 ``sharded_greedy_sort`` (multi-GPU). All arithmetic runs in libskr.so
 (hand-written sm_100a CUDA); there is no CPU fallback.
@@ -18,10 +18,16 @@ from .gcrodr import (
 )
 from .gmres import SolveReport, SolverConfig, gmres_solve
 from .precond import (
+    BlockJacobiPreconditioner,
+    DevicePreconditioner,
+    Icc0Preconditioner,
     IdentityPreconditioner,
+    Ilu0Preconditioner,
     JacobiPreconditioner,
     Preconditioner,
+    SorPreconditioner,
     ZeroPivotError,
+    build_device_preconditioner,
     build_preconditioner,
 )
 from .sequence import (
@@ -49,6 +55,8 @@ from .sparse import CsrMatrix, DeviceCsr, axpy, dot, eye, norm2, spmv
 __version__ = "0.1.0"
 
 __all__ = [
+    "BlockJacobiPreconditioner", "DevicePreconditioner", "Icc0Preconditioner", "Ilu0Preconditioner",
+    "SorPreconditioner", "build_device_preconditioner",
     "ChainState", "CsrMatrix", "DeviceCsr", "GcroDrEngine", "IdentityPreconditioner", "JacobiPreconditioner",
     "ParameterMatrix", "Preconditioner", "RecycleSpace", "SequenceResult", "SolveReport",
     "SolverConfig", "ZeroPivotError", "axpy", "build_preconditioner", "chunk_positions", "dot",

@@ -21,8 +21,8 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libskr.so")
 HOSTLIB = os.path.join(PKG, "libskr_hostdense.so")
 
-CUDA_SOURCES = ["gcrodr.cu", "sort.cu", "assemble.cu", "grf.cu"]
-HEADERS = ["dense.h", "recycle.h", "skr_device.cuh"]
+CUDA_SOURCES = ["gcrodr.cu", "sort.cu", "assemble.cu", "grf.cu", "precond.cu"]
+HEADERS = ["dense.h", "recycle.h", "skr_device.cuh", "precond.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -24,6 +24,7 @@ EXPORTS = (
     "skr_gcrodr_profile", "skr_gcrodr_solve_chains", "skr_gcrodr_diagnostics",
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
     "skr_greedy_sort", "skr_dense_hr_first", "skr_dense_hr_next",
+    "skr_precond_bytes", "skr_precond_build", "skr_precond_apply",
 )
 
 
@@ -34,7 +35,8 @@ class SkrExtensionError(RuntimeError):
 class SkrCsr(ctypes.Structure):
     _fields_ = [("n", c_int32), ("nnz", c_int32), ("row_ptr", c_void_p),
                 ("col_idx", c_void_p), ("values", c_void_p), ("diag", c_void_p),
-                ("stencil", c_void_p), ("sx", c_int32), ("sxy", c_int32)]
+                ("stencil", c_void_p), ("sx", c_int32), ("sxy", c_int32),
+                ("precond", c_void_p)]
 
 
 class SkrSystem(ctypes.Structure):
@@ -60,6 +62,8 @@ class SkrReport(ctypes.Structure):
                 ("dense_kernel_ms", c_double), ("launches", c_int32),
                 ("arnoldi_steps", c_int32)]
 
+
+PC_KINDS = {"sor": 1, "ilu0": 2, "icc0": 3, "bjacobi": 4}
 
 WARN_SINGULAR_H = 1
 WARN_SINGULAR_CROSS = 2
@@ -114,6 +118,10 @@ def _declare(L):
                                c_int32),
         "skr_dense_hr_next": ([P, c_int32, P, c_int32, c_int32, c_int32, P, c_int32,
                                POINTER(c_int32), P], c_int32),
+        "skr_precond_bytes": ([c_int32, c_int32, c_int32, c_int32], c_size_t),
+        "skr_precond_build": ([POINTER(SkrCsr), c_int32, c_double, c_int32, P, c_size_t,
+                               POINTER(c_int32), POINTER(c_double), P], c_int32),
+        "skr_precond_apply": ([P, P, P, c_int32, c_int64, c_int64, P], c_int32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

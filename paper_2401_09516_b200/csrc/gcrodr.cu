@@ -28,6 +28,7 @@
 #include <thread>
 #include <vector>
 
+#include "precond.cuh"
 #include "recycle.h"
 #include "skr_device.cuh"
 
@@ -173,6 +174,10 @@ struct Ptrs {
   double v0_rtol;  // |C^T r| / beta above which V_0 is formed from r - C C^T r (V0_PROJ_RTOL)
   int fuse_comb;  // 1: k_cycle applies the recycle update at its start (large row slices);
                   // 0: a separate k_combine launch after every dense update
+  int gram_half;  // 1: the DMMA cross-Gram computes What^T U only (What^T V = [0; I])
+  PcHeader* pch;  // general preconditioner (SOR / ILU0 / IC0 / block Jacobi) or nullptr; with
+                  // it dg is nullptr and op(v) = M^-1 (A v) runs as an SpMV phase followed by
+                  // the level-scheduled sweeps of precond.cuh
 };
 
 __device__ __forceinline__ double* colU(const Ptrs& p, int c) { return p.basis + (size_t)c * p.ld; }
@@ -427,6 +432,71 @@ __global__ void __launch_bounds__(NT) k_project(Ptrs p) {
   double t = block_sum(rr, s_red);
   if (threadIdx.x == 0) p.part[(size_t)(2 * kc) * GRID_MAX + blockIdx.x] = t;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->comb_part = 0;
+}
+
+
+// ---------------------------------------------------------------------------
+// general preconditioner outside the cycle kernel (cooperative, nblk CTAs, the
+// solve's own barrier words): M^-1 applied in place to
+//   target 0  r (and M^-1 b into z when x0 is given), then the |M^-1 b|^2 and
+//             |r|^2 partials k_init left unpreconditioned (gcrodr.py:348-351)
+//   target 1  W = op(Yo): the C block columns k_spmm wrote (gcrodr.py:96)
+//   target 2  op(U) into the V block for the diagnostics record (gcrodr.py:116-123)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool diag_skip(const State* st, int stage);
+__global__ void __launch_bounds__(NT) k_pc_cols(Ptrs p, int target, int stage) {
+  State* st = p.st;
+  __shared__ PcView s_pc;
+  __shared__ int s_flag;
+  __shared__ double s_red[NW];
+  const int tid = threadIdx.x, blk = blockIdx.x;
+  if (tid == 0) s_pc = p.pch->v;
+  __syncthreads();
+  unsigned long long seen =
+      tid == 0 ? ld_relaxed_gpu64(&st->bar_count) / (unsigned long long)p.nblk : 0ull;
+  auto sync = [&]() -> bool {
+    return grid_sync(&st->bar_count, &st->abort_flag, p.nblk, &s_flag, seen);
+  };
+  auto fail = [&]() {
+    if (tid == 0) {
+      st->done = 1;
+      if (blk == 0) flag_host(st, -1, 1);
+    }
+  };
+  const int r0 = blk * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  if (target == 0) {
+    const bool hx = st->has_x0 != 0;
+    if (hx) {
+      for (int row = r0 + tid; row < r1; row += NT) p.z[row] = __ldg(p.b + row);
+      if (!sync()) return fail();
+      if (!pc_apply_grid(s_pc, p.z, 1, 0, sync)) return fail();
+    }
+    if (!pc_apply_grid(s_pc, p.r, 1, 0, sync)) return fail();
+    double sr = 0.0, sbp = 0.0;
+    for (int row = r0 + tid; row < r1; row += NT) {
+      const double rv = p.r[row], bp = hx ? p.z[row] : rv;
+      sr += rv * rv;
+      sbp += bp * bp;
+    }
+    const double t1 = block_sum(sbp, s_red);
+    const double t2 = block_sum(sr, s_red);
+    if (tid == 0) {
+      p.part[1 * GRID_MAX + blk] = t1;
+      p.part[2 * GRID_MAX + blk] = t2;
+    }
+  } else if (target == 1) {
+    const int r = st->ncol_a;
+    if (st->done || r <= 0) return;
+    if (!pc_apply_grid(s_pc, colC(p, p.kcap - r), r, p.ld, sync)) return fail();
+  } else {
+    if (diag_skip(st, stage)) return;
+    const int kc = st->kc;
+    const bool sten = sten_ok(p.sv);
+    for (int row = r0 + tid; row < r1; row += NT)
+      for (int q = 0; q < kc; ++q) colV(p, q)[row] = op_row(p, sten, colU(p, q), row);
+    if (!sync()) return fail();
+    if (!pc_apply_grid(s_pc, colV(p, 0), kc, p.ld, sync)) return fail();
+  }
 }
 
 // true residual partials |b - A x|^2
@@ -743,13 +813,19 @@ constexpr size_t CYCLE_DSMEM_BUDGET = SKR_CYCLE_DSMEM_KB * 1024;
 
 // R = rows per lane in the Arnoldi sweeps: warp-owned tiles of 32 R consecutive
 // rows; every lane keeps its rows' w = V_t and z = op(V_t) in registers.
-template <int R>
 #ifndef SKR_CYCLE_MINB
 #define SKR_CYCLE_MINB 2  // CTAs per SM the register allocation must allow
 #endif
+// GPC: a general preconditioner (p.pch) instead of none / Jacobi.
+template <int R, bool GPC>
 __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
   State* st = p.st;
   __shared__ CycleSmem S;
+  __shared__ PcView s_pc;
+  if (GPC) {
+    if (threadIdx.x == 0) s_pc = p.pch->v;
+    __syncthreads();
+  }
   extern __shared__ double cdyn[];
   // offsets from the host (cycle_smem_layout): kernel parameters, not registers
   double* gtile = cdyn;          // Gram tile, column-major, ld GT_LD
@@ -767,6 +843,13 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   int* abt = &st->abort_flag;
   // completed grid barriers of this solve (no barrier is in flight at launch)
   unsigned long long bar_seen = tid == 0 ? ld_relaxed_gpu64(bc) / (unsigned long long)nblk : 0ull;
+  auto cycle_sync = [&]() -> bool { return grid_sync(bc, abt, nblk, &S.flag, bar_seen); };
+  auto cycle_abort = [&]() {
+    if (tid == 0) {
+      st->done = 1;
+      if (blk == 0) flag_host(st, cycle_id, 1);
+    }
+  };
 
   // ---- the previous cycle's recycle update (gcrodr.py:444-467), in place ------
   // U <- [U | V_0..V_{j-1}] coefU, C <- [C | V_0..V_j] coefC (coefficients of
@@ -984,11 +1067,13 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   const bool nbsync = halo >= 0 && 2 * halo + 1 < nblk && 2 * halo + 1 <= NT;
   // ---- cycle start --------------------------------------------------------
   const bool pend = p.fuse_comb && st->comb_pending != 0;
+  long long cprof_t = clock64();
   if (pend) {
     apply_update(defl);
     CYCLE_SYNC();  // every CTA has read comb_pending and written its partials
     if (blk == 0 && tid == 0) st->comb_pending = 0;
   }
+  CPROF(12);
   // partials: this launch's update (pend), k_project after a refresh
   // (comb_part 0), or a k_combine (comb_part 1)
   const bool comb_part = pend || st->comb_part != 0;
@@ -1060,12 +1145,12 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 #endif
   int red_idx = 0;
   CYCLE_SYNC();
+  CPROF(13);
 
   int j = 0;
   bool brk = false;
   double wn0_pending = 0.0;  // ||w - C C^T w|| / eta of the pending vector's step
   double hres = beta0;
-  long long cprof_t = clock64();
   for (int t = 0; t <= s; ++t) {
     const bool do_spmv = (t < s);
     const int pb = kc + t;  // final basis columns [C | v_0..v_{t-1}]
@@ -1074,6 +1159,15 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     // no block barrier inside: each warp streams its own tiles, the basis
     // columns in batches of CB (CB R independent loads per lane in flight), and
     // reduce-scatters the 2 CB partial dots of a batch with one butterfly.
+    if (GPC && do_spmv) {
+      // z = M^-1 (A V_t): the SpMV over this CTA's rows, then the grid-wide sweeps
+      for (int row = r0 + tid; row < r1; row += NT) p.z[row] = row_dot(Vt, row);
+      CYCLE_SYNC();
+      if (!pc_apply_grid(s_pc, p.z, 1, 0, cycle_sync)) {
+        cycle_abort();
+        return;
+      }
+    }
     double* sw = sacc + warp * 2 * PVC;
     for (int c = lane; c < 2 * PVC; c += 32) sw[c] = 0.0;
     __syncwarp();
@@ -1093,7 +1187,10 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       double dgv[R];  // Jacobi pivots, loaded ahead of the SpMV's dependent chain
 #pragma unroll
       for (int i = 0; i < R; ++i) dgv[i] = p.dg ? __ldg(p.dg + row[i]) : 1.0;
-      if (do_spmv) {
+      if (do_spmv && GPC) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) z[i] = p.z[row[i]];  // M^-1 A V_t of the phase above
+      } else if (do_spmv) {
         if (sten_local) {
 #pragma unroll
           for (int i = 0; i < R; ++i)
@@ -1497,6 +1594,10 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     constexpr int GL = GM_LD;  // == 4 (mod 16) doubles: conflict-free fragment loads
     const int ncs = 2 * kc + j;
     const int nb = (mm + 7) >> 3;  // 8 x 8 blocks per side, <= 5
+    // Vhat block columns the tensor cores compute: all of them, or (gram_half)
+    // only those holding U columns -- What^T V = [0; I] is then taken from the
+    // orthonormality DCGS2 maintains (see the cross reduction below)
+    const int nby = p.gram_half ? (kc + 7) >> 3 : nb;
     // warp w: block rows bi in [3 h, 3 h + 3) (h = w & 1), k-steps 2 (w >> 1)
     // and 2 (w >> 1) + 1 of every tile (rows 4 ks .. 4 ks + 3); lane l holds
     // A[m = l/4][k = l%4] = What(row, 8 bi + m), B[k][n = l/4] = Vhat(row, 8 bj + n)
@@ -1564,13 +1665,14 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 #pragma unroll
         for (int x = 0; x < 3; ++x) af[x] = gtl[wa[x] + roff];
 #pragma unroll
-        for (int y = 0; y < 5; ++y) bf[y] = gtl[vb[y] + roff];
+        for (int y = 0; y < 5; ++y)
+          if (y < nby) bf[y] = gtl[vb[y] + roff];
 #pragma unroll
         for (int x = 0; x < 3; ++x)
           if (3 * h + x < nb)
 #pragma unroll
             for (int y = 0; y < 5; ++y)
-              if (y < nb)
+              if (y < nby)
                 asm volatile(
                     "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                     : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
@@ -1595,7 +1697,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
 #pragma unroll
           for (int y = 0; y < 5; ++y) {
             const int bi = 3 * h + x;
-            if (bi < nb && y < nb) {
+            if (bi < nb && y < nby) {
               const int idx = (bi * nb + y) * 64 + ln * 8 + 2 * lk;
               if (q < 2) {
                 gb[idx] = acc[x][y][0];
@@ -1609,7 +1711,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       }
       __syncthreads();
     }
-    for (int e = tid; e < mm * mm; e += NT) {
+    for (int e = tid; e < mm * (p.gram_half ? kc : mm); e += NT) {
       const int a = e % mm, b = e / mm;
       p.part[(size_t)(GRAM_PART0 + e) * GRID_MAX + blk] =
           gb[((a >> 3) * nb + (b >> 3)) * 64 + (a & 7) * 8 + (b & 7)];
@@ -1633,6 +1735,15 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     if (p.dg) rv = __ddiv_rn(rv, __ldg(p.dg + row));
     p.r[row] = rv;
     rr += rv * rv;
+  }
+  if (GPC) {
+    CYCLE_SYNC();
+    if (!pc_apply_grid(s_pc, p.r, 1, 0, cycle_sync)) {
+      cycle_abort();
+      return;
+    }
+    rr = 0.0;
+    for (int row = r0 + tid; row < r1; row += NT) rr = fma(p.r[row], p.r[row], rr);
   }
   if (defl && !gmma) {
     // cross-Gram What[:, :mm]^T Vhat over this CTA's rows, register-tiled: a
@@ -1745,15 +1856,20 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     // one warp per cross entry: sum the CTAs' partials (lane-strided, then a
     // butterfly: a fixed order), scale Vhat's U columns by dk (Vhat =
     // [U diag(dk), V]) into st->cross
+    const bool half = gmma && p.gram_half;
     for (int e = blk * NW + warp; e < mm * mm; e += nblk * NW) {
+      const int a = e % mm, b = e / mm;
+      if (half && b >= kc) {
+        // What^T V_{b - kc}: [C | V] is orthonormal (DCGS2 + the V_0 projection
+        // keep ||Q^T Q - I|| at 1e-13), so the column is e_b
+        if (lane == 0) st->cross[a + b * LDX] = a == b ? 1.0 : 0.0;
+        continue;
+      }
       const double* q = p.part + (size_t)(GRAM_PART0 + e) * GRID_MAX;
       double v = 0.0;
       for (int c = lane; c < nblk; c += 32) v += q[c];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) {
-        const int a = e % mm, b = e / mm;
-        st->cross[a + b * LDX] = (b < kc) ? v * st->dk[b] : v;
-      }
+      if (lane == 0) st->cross[a + b * LDX] = (b < kc) ? v * st->dk[b] : v;
     }
   }
   if (blk == 0) {
@@ -1815,7 +1931,8 @@ __global__ void __launch_bounds__(NT) k_diag(Ptrs p, int stage) {
   for (int row = r0 + threadIdx.x; row < r1; row += NT) {
     const double d = p.dg ? __ldg(p.dg + row) : 1.0;
     for (int q = 0; q < kc; ++q) {
-      double v = op_row(p, sten, colU(p, q), row);
+      // general preconditioner: op(U_q) was formed in the V block (k_pc_cols target 2)
+      double v = p.pch ? colV(p, q)[row] : op_row(p, sten, colU(p, q), row);
       if (p.dg) v = __ddiv_rn(v, d);
       v -= colC(p, p.kcap - kc + q)[row];
       res += v * v;
@@ -2199,9 +2316,10 @@ static std::mutex g_mu;
 // k_cycle instantiation for R rows per lane (1, 2 or 4)
 static const void* cycle_kernel(int R) {
   switch (R) {
-    case 1: return (const void*)k_cycle<1>;
-    case 2: return (const void*)k_cycle<2>;
-    default: return (const void*)k_cycle<4>;
+    case 1: return (const void*)k_cycle<1, false>;
+    case 2: return (const void*)k_cycle<2, false>;
+    case 4: return (const void*)k_cycle<4, false>;
+    default: return (const void*)k_cycle<2, true>;  // general preconditioner
   }
 }
 
@@ -2232,7 +2350,7 @@ static int ensure_dev(DevInfo** out) {
                              (int)dense_smem_bytes()) != cudaSuccess)
       return SKR_ERR_CUDA;
     int nb = 1 << 30;
-    for (int v = 0; v < 3; ++v) {
+    for (int v = 0; v < 4; ++v) {
       const void* f = cycle_kernel(1 << v);
       if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)CYCLE_DSMEM_BUDGET) != cudaSuccess)
@@ -2415,10 +2533,12 @@ int skr_spmv(const skr_csr* A, const double* x, double* y, int apply_prec, void*
   if (!A || A->n < 0 || (A->n > 0 && (!x || !y || !A->row_ptr))) return SKR_ERR_ARG;
   if (A->n == 0) return SKR_OK;
   int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
+  const bool gpc = apply_prec && A->precond;
   k_spmv<<<grid, NT, 0, (cudaStream_t)stream>>>(A->n, A->row_ptr, A->col_idx, A->values,
-                                                 apply_prec ? A->diag : nullptr, stencil_of(A), x,
-                                                 y);
-  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+                                                 apply_prec && !gpc ? A->diag : nullptr,
+                                                 stencil_of(A), x, y);
+  if (cudaGetLastError() != cudaSuccess) return SKR_ERR_CUDA;
+  return gpc ? skr_precond_apply(A->precond, y, y, 1, A->n, A->n, stream) : SKR_OK;
 }
 
 int skr_residual(const skr_csr* A, const double* b, const double* x, double* r, int apply_prec,
@@ -2426,10 +2546,12 @@ int skr_residual(const skr_csr* A, const double* b, const double* x, double* r, 
   if (!A || A->n < 0) return SKR_ERR_ARG;
   if (A->n == 0) return SKR_OK;
   int grid = std::min(148 * 8, (A->n + NT - 1) / NT);
+  const bool gpc = apply_prec && A->precond;
   k_resid<<<grid, NT, 0, (cudaStream_t)stream>>>(A->n, A->row_ptr, A->col_idx, A->values,
-                                                  apply_prec ? A->diag : nullptr, stencil_of(A), b,
-                                                  x, r);
-  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+                                                  apply_prec && !gpc ? A->diag : nullptr,
+                                                  stencil_of(A), b, x, r);
+  if (cudaGetLastError() != cudaSuccess) return SKR_ERR_CUDA;
+  return gpc ? skr_precond_apply(A->precond, r, r, 1, A->n, A->n, stream) : SKR_OK;
 }
 
 size_t skr_gcrodr_workspace_bytes(int32_t n, int32_t m, int32_t k, int32_t max_iter) {
@@ -2478,7 +2600,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.rp = A->row_ptr;
   p.ci = A->col_idx;
   p.av = A->values;
-  p.dg = A->diag;
+  p.pch = (PcHeader*)A->precond;
+  p.dg = p.pch ? nullptr : A->diag;  // a general preconditioner replaces the Jacobi diagonal
   p.sv = stencil_of(A);
   p.b = b;
   p.x = x;
@@ -2494,6 +2617,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   p.ld = L.ld;
   p.kcap = L.kcap;
   const int nblk = cfg_nblk(*d, n, cfg->grid_ctas);
+  int launches_pc = 0;
   p.nblk = nblk;
   p.rpb = (int)align_up((size_t)((n + nblk - 1) / nblk), 32);
   // the in-kernel (tensor-core) recycle update pays off when the row slices
@@ -2503,6 +2627,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   if (const char* e = getenv("SKR_FUSE_COMB")) p.fuse_comb = atoi(e) ? 1 : 0;
   p.v0_rtol = V0_PROJ_RTOL;
   if (const char* e = getenv("SKR_V0_RTOL")) p.v0_rtol = atof(e);
+  p.gram_half = 0;
+  if (const char* e = getenv("SKR_GRAM_HALF")) p.gram_half = atoi(e) ? 1 : 0;
   const bool diag = (cfg->flags & SKR_COLLECT_DIAGNOSTICS) != 0;
   if (diag) p.fuse_comb = 0;  // the update is applied before each record
   const int kt = L.kcap;
@@ -2524,7 +2650,15 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   }
   size_t cycle_dsmem = cycle_fixed + csr_cap;
   int csr_cap_i = (int)csr_cap;
-  const void* cycle_fn = cycle_kernel(cycle_rows_per_lane(p.rpb));
+  const void* cycle_fn = cycle_kernel(p.pch ? 8 : cycle_rows_per_lane(p.rpb));
+  int pc_target = 0, pc_stage = 0;
+  void* pcargs[3] = {&p, &pc_target, &pc_stage};
+  auto launch_pc = [&](int target, int stage) {
+    pc_target = target;
+    pc_stage = stage;
+    ++launches_pc;
+    return cudaLaunchCooperativeKernel((const void*)k_pc_cols, dim3(nblk), dim3(NT), pcargs, 0, s);
+  };
   // k_combine is latency-bound per row: run it on >= 2 CTAs per SM (its
   // next-cycle partials are folded into nblk slots, so the grid is free)
   const int ncomb = std::max(1, std::min(std::min(GRID_MAX, std::max(nblk, 2 * d->sms)),
@@ -2548,6 +2682,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
                       (size_t)n * sizeof(double), k_eff, cudaMemcpyDeviceToDevice, s);
   }
   k_init<<<nblk, NT, 0, s>>>(p, x0);
+  if (p.pch) launch_pc(0, 0);
   const size_t dsm = dense_smem_bytes(cfg->m);
   k_dense<<<1, NT, dsm, s>>>(p, P_INIT, 0, -1);
   launches += 3;
@@ -2563,6 +2698,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     launch_combine(kt, p, ncomb, 0, s);
     // W = op(Yo) into the C block; QRCP(W) -> C, U
     k_spmm<<<nblk, NT, 0, s>>>(p);
+    if (p.pch) launch_pc(1, 0);
     k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
     k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 1, -1);
@@ -2578,6 +2714,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     k_dense<<<1, NT, dsm, s>>>(p, P_PROJ_FIN, 0, -1);
     launches += 21;
     if (diag) {
+      if (p.pch) launch_pc(2, 0);
       k_diag<<<nblk, NT, 0, s>>>(p, 0);
       k_diag_fin<<<1, NT, 0, s>>>(p, 0);
       launches += 2;
@@ -2631,6 +2768,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
         ++launches;
       }
       if (diag) {
+        if (p.pch) launch_pc(2, 1);
         k_diag<<<nblk, NT, 0, s>>>(p, 1);
         k_diag_fin<<<1, NT, 0, s>>>(p, 1);
         launches += 2;
@@ -2723,7 +2861,7 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   rep->spmv_ortho_bytes = hs.step_bytes;
   rep->cycle_kernel_ms = cyc_ms;
   rep->dense_kernel_ms = den_ms;
-  rep->launches = launches;
+  rep->launches = launches + launches_pc;
   rep->arnoldi_steps = hs.steps;
   if (hist && hist_cap > 0)
     cudaMemcpyAsync(hist, p.hist, sizeof(double) * std::min(hist_cap, hs.hist_len),

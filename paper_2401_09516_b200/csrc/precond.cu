@@ -1,0 +1,541 @@
+// Device build and standalone apply of the general left preconditioners
+// (kryrec/precond.py:80-145 classes, :161-248 factorizations, :251-312
+// build_preconditioner): SOR, ILU(0), IC(0), block Jacobi. See precond.cuh
+// for the layout and the sweep. Everything here is one cooperative kernel per
+// call: the symbolic analysis (dependency levels of the lower and the upper
+// pattern by monotone relaxation, counting sort of the rows by level) and the
+// numeric factorization (level by level, every row one thread, the reference's
+// operation order: IKJ ILU(0) with separate multiply and subtract; IC(0) row by
+// row with the reference's running sums).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "precond.cuh"
+
+namespace skr {
+
+struct PcLayout {
+  size_t fval, dpos, lptr[2], lrows[2], lev[2], cur[2], lu, perm, total;
+};
+
+static inline size_t pc_align(size_t x) { return (x + 255) / 256 * 256; }
+
+constexpr size_t PC_HEADER_BYTES = 1024;  // the factor starts here (precond.py reads it back)
+static_assert(sizeof(PcHeader) <= PC_HEADER_BYTES, "preconditioner header");
+
+static PcLayout pc_layout(int kind, int n, int nnz, int bs) {
+  PcLayout L{};
+  size_t off = PC_HEADER_BYTES;
+  if (kind == PC_BJACOBI) {
+    const size_t nb = ((size_t)n + bs - 1) / bs;
+    L.lu = off;
+    off = pc_align(off + nb * bs * bs * sizeof(double));
+    L.perm = off;
+    off = pc_align(off + (size_t)n * sizeof(int));
+  } else {
+    L.fval = off;
+    off = pc_align(off + (size_t)nnz * sizeof(double));
+    L.dpos = off;
+    off = pc_align(off + (size_t)n * sizeof(int));
+    for (int h = 0; h < 2; ++h) {
+      L.lptr[h] = off;
+      off = pc_align(off + ((size_t)n + 2) * sizeof(int));
+      L.lrows[h] = off;
+      off = pc_align(off + (size_t)n * sizeof(int));
+      L.lev[h] = off;
+      off = pc_align(off + (size_t)n * sizeof(int));
+      L.cur[h] = off;
+      off = pc_align(off + ((size_t)n + 2) * sizeof(int));
+    }
+  }
+  L.total = off;
+  return L;
+}
+
+struct PcBuildArgs {
+  PcHeader* h;
+  int kind, n;
+  const int* rp;
+  const int* ci;
+  const double* av;
+  double omega;
+  double* fval;
+  int* dpos;
+  int* lptr[2];
+  int* lrows[2];
+  int* lev[2];
+  int* cur[2];
+  int bs, nb;
+  double* lu;
+  int* perm;
+};
+
+__device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
+
+// position of column j in [q0, q1) of the sorted row, or -1
+__device__ __forceinline__ int find_col(const int* ci, int q0, int q1, int j) {
+  while (q0 < q1) {
+    const int mid = (q0 + q1) >> 1;
+    const int c = __ldg(ci + mid);
+    if (c == j) return mid;
+    if (c < j)
+      q0 = mid + 1;
+    else
+      q1 = mid;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void pc_error(PcHeader* h, int status, int row, double value) {
+  // the smallest row wins (the reference stops at the first one it meets)
+  const int old = atomicMin(&h->err_row, row);
+  if (row < old) {
+    h->err_value = value;  // racy among equal rows only
+    atomicMax(&h->status, status);
+  }
+}
+
+// exclusive scan of cnt[0 .. len) by one CTA into out[0 .. len] (out[len] = total)
+__device__ void cta_scan(const int* cnt, int* out, int len, int* s_tmp) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int chunk = (len + nt - 1) / nt;
+  const int a = min(len, tid * chunk), b = min(len, a + chunk);
+  int s = 0;
+  for (int q = a; q < b; ++q) s += cnt[q];
+  s_tmp[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int q = 0; q < nt; ++q) {
+      const int t = s_tmp[q];
+      s_tmp[q] = run;
+      run += t;
+    }
+    out[len] = run;
+  }
+  __syncthreads();
+  int run = s_tmp[tid];
+  for (int q = a; q < b; ++q) {
+    const int t = cnt[q];
+    out[q] = run;
+    run += t;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT) k_pc_build(PcBuildArgs a) {
+  PcHeader* h = a.h;
+  __shared__ int s_flag;
+  __shared__ int s_tmp[NT];
+  const int n = a.n;
+  const int tid = threadIdx.x;
+  const int gtid = blockIdx.x * NT + tid, gthreads = gridDim.x * NT;
+  unsigned long long seen = 0ull;  // the header (and its counter) is zeroed before the launch
+  auto sync = [&]() -> bool { return grid_sync(&h->bar_count, &h->abort_flag, gridDim.x, &s_flag, seen); };
+#define PC_SYNC()                                   \
+  do {                                              \
+    if (!sync()) {                                  \
+      if (gtid == 0) h->status = PCS_ABORTED;       \
+      return;                                       \
+    }                                               \
+  } while (0)
+
+  if (a.kind == PC_BJACOBI) {
+    // ---- dense LU with partial pivoting of every diagonal block, one warp each
+    const int lane = tid & 31;
+    const int gw = gtid >> 5, nw = gthreads >> 5;
+    const int bs = a.bs;
+    for (int b = gw; b < a.nb; b += nw) {
+      const int start = b * bs, bsz = min(bs, n - start);
+      double* A = a.lu + (size_t)b * bs * bs;
+      for (int e = lane; e < bs * bs; e += 32) A[e] = 0.0;
+      for (int e = lane; e < bsz; e += 32) a.perm[start + e] = e;
+      __syncwarp();
+      for (int i = 0; i < bsz; ++i) {
+        const int q0 = __ldg(a.rp + start + i), q1 = __ldg(a.rp + start + i + 1);
+        for (int q = q0 + lane; q < q1; q += 32) {
+          const int c = __ldg(a.ci + q) - start;
+          if (c >= 0 && c < bsz) A[i + (size_t)c * bs] = __ldg(a.av + q);
+        }
+      }
+      __syncwarp();
+      for (int k = 0; k < bsz; ++k) {
+        // pivot: the first row of the largest |A[i, k]|, i >= k (idamax)
+        double best = -1.0;
+        int bi = bsz;
+        for (int i = k + lane; i < bsz; i += 32) {
+          const double t = fabs(A[i + (size_t)k * bs]);
+          if (t > best) {
+            best = t;
+            bi = i;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (bi != k) {
+          for (int c = lane; c < bsz; c += 32) {
+            const double t = A[k + (size_t)c * bs];
+            A[k + (size_t)c * bs] = A[bi + (size_t)c * bs];
+            A[bi + (size_t)c * bs] = t;
+          }
+          if (lane == 0) {
+            const int t = a.perm[start + k];
+            a.perm[start + k] = a.perm[start + bi];
+            a.perm[start + bi] = t;
+          }
+        }
+        __syncwarp();
+        const double piv = A[k + (size_t)k * bs];
+        if (piv == 0.0) {
+          if (lane == 0) pc_error(h, PCS_ZERO_PIVOT, start + k, 0.0);
+          continue;  // LAPACK goes on with the other columns (info > 0)
+        }
+        const double rp_ = 1.0 / piv;
+        for (int i = k + 1 + lane; i < bsz; i += 32) A[i + (size_t)k * bs] *= rp_;
+        __syncwarp();
+        for (int c = k + 1; c < bsz; ++c) {
+          const double akc = A[k + (size_t)c * bs];
+          for (int i = k + 1 + lane; i < bsz; i += 32)
+            A[i + (size_t)c * bs] =
+                __dsub_rn(A[i + (size_t)c * bs], __dmul_rn(A[i + (size_t)k * bs], akc));
+        }
+        __syncwarp();
+      }
+    }
+    if (gtid == 0) {
+      PcView& v = h->v;
+      v.kind = PC_BJACOBI;
+      v.n = n;
+      v.nsweep = 0;
+      v.scale = 1.0;
+      v.bs = bs;
+      v.nb = a.nb;
+      v.lu = a.lu;
+      v.perm = a.perm;
+    }
+    return;
+  }
+
+  // ---- S0: diagonal positions, factor values, zero levels ------------------
+  for (int i = gtid; i < n; i += gthreads) {
+    const int q0 = __ldg(a.rp + i), q1 = __ldg(a.rp + i + 1);
+    const int d = find_col(a.ci, q0, q1, i);
+    a.dpos[i] = d;
+    const double dv = d >= 0 ? __ldg(a.av + d) : 0.0;
+    if (dv == 0.0) pc_error(h, PCS_ZERO_PIVOT, i, 0.0);
+    if (!(dv < 0.0)) h->any_nonneg_diag = 1;
+    for (int q = q0; q < q1; ++q) {
+      double t = __ldg(a.av + q);
+      if (a.kind == PC_SOR && q == d) t = __ddiv_rn(t, a.omega);
+      a.fval[q] = t;
+    }
+    a.lev[0][i] = 0;
+    a.lev[1][i] = 0;
+  }
+  for (int i = gtid; i < n + 2; i += gthreads) {
+    a.cur[0][i] = 0;
+    a.cur[1][i] = 0;
+  }
+  PC_SYNC();
+  if (vload(&h->err_row) < n) return;
+  const bool need_up = a.kind != PC_SOR;
+  // ---- S1: dependency levels, monotone relaxation to the least fixed point --
+  for (int it = 0;; ++it) {
+    int changed = 0;
+    for (int i = gtid; i < n; i += gthreads) {
+      const int d = a.dpos[i];
+      int l = 0;
+      for (int q = __ldg(a.rp + i); q < d; ++q) l = max(l, vload(a.lev[0] + __ldg(a.ci + q)) + 1);
+      if (l != a.lev[0][i]) {
+        a.lev[0][i] = l;
+        changed = 1;
+      }
+      if (need_up) {
+        int u = 0;
+        for (int q = d + 1; q < __ldg(a.rp + i + 1); ++q)
+          u = max(u, vload(a.lev[1] + __ldg(a.ci + q)) + 1);
+        if (u != a.lev[1][i]) {
+          a.lev[1][i] = u;
+          changed = 1;
+        }
+      }
+    }
+    if (__syncthreads_or(changed) && tid == 0) atomicExch(&h->chg[it % 3], 1);
+    if (gtid == 0) h->chg[(it + 1) % 3] = 0;
+    PC_SYNC();
+    if (vload(&h->chg[it % 3]) == 0) break;
+  }
+  // ---- S2: level histogram ---------------------------------------------------
+  for (int i = gtid; i < n; i += gthreads) {
+    const int l = a.lev[0][i];
+    atomicAdd(a.cur[0] + l, 1);
+    atomicMax(&h->maxlev[0], l);
+    if (need_up) {
+      const int u = a.lev[1][i];
+      atomicAdd(a.cur[1] + u, 1);
+      atomicMax(&h->maxlev[1], u);
+    }
+  }
+  PC_SYNC();
+  const int nlev0 = vload(&h->maxlev[0]) + 1, nlev1 = need_up ? vload(&h->maxlev[1]) + 1 : 0;
+  // ---- S3: level pointers (CTA 0: lower, CTA 1 or 0: upper) ------------------
+  if (blockIdx.x == 0) cta_scan(a.cur[0], a.lptr[0], nlev0, s_tmp);
+  if (need_up && blockIdx.x == (gridDim.x > 1 ? 1 : 0)) cta_scan(a.cur[1], a.lptr[1], nlev1, s_tmp);
+  PC_SYNC();
+  for (int l = gtid; l < nlev0; l += gthreads) a.cur[0][l] = a.lptr[0][l];
+  if (need_up)
+    for (int l = gtid; l < nlev1; l += gthreads) a.cur[1][l] = a.lptr[1][l];
+  PC_SYNC();
+  // ---- S4: rows into their levels ---------------------------------------------
+  for (int i = gtid; i < n; i += gthreads) {
+    a.lrows[0][atomicAdd(a.cur[0] + a.lev[0][i], 1)] = i;
+    if (need_up) a.lrows[1][atomicAdd(a.cur[1] + a.lev[1][i], 1)] = i;
+  }
+  PC_SYNC();
+  // ---- S5: numeric factorization, level by level -------------------------------
+  const double sign = (a.kind == PC_ICC0 && !vload(&h->any_nonneg_diag)) ? -1.0 : 1.0;
+  if (a.kind == PC_ILU0 || a.kind == PC_ICC0) {
+    if (a.kind == PC_ICC0) {
+      // the reference asks for a symmetric matrix, pattern and values (precond.py:303-304)
+      for (int i = gtid; i < n; i += gthreads) {
+        const int d = a.dpos[i];
+        for (int q = __ldg(a.rp + i); q < d; ++q) {
+          const int j = __ldg(a.ci + q);
+          const int m = find_col(a.ci, a.dpos[j] + 1, __ldg(a.rp + j + 1), i);
+          if (m < 0 || __ldg(a.av + m) != __ldg(a.av + q)) atomicMax(&h->status, PCS_NOT_SYMMETRIC);
+        }
+        for (int q = d + 1; q < __ldg(a.rp + i + 1); ++q) {
+          const int j = __ldg(a.ci + q);
+          if (find_col(a.ci, __ldg(a.rp + j), a.dpos[j], i) < 0)
+            atomicMax(&h->status, PCS_NOT_SYMMETRIC);
+        }
+      }
+      PC_SYNC();
+      if (vload(&h->status) == PCS_NOT_SYMMETRIC) return;
+    }
+    for (int l = 0; l < nlev0; ++l) {
+      const int lo = a.lptr[0][l], hi = a.lptr[0][l + 1];
+      for (int e = lo + gtid; e < hi; e += gthreads) {
+        const int i = a.lrows[0][e];
+        const int q0 = __ldg(a.rp + i), q1 = __ldg(a.rp + i + 1), d = a.dpos[i];
+        if (a.kind == PC_ILU0) {
+          // IKJ on the row's own pattern (precond.py:178-193)
+          for (int p = q0; p < d; ++p) {
+            const int k = __ldg(a.ci + p);
+            const int dk = a.dpos[k];
+            const double pivot = a.fval[dk];
+            if (pivot == 0.0) pc_error(h, PCS_ZERO_PIVOT, k, 0.0);
+            const double lik = __ddiv_rn(a.fval[p], pivot);
+            a.fval[p] = lik;
+            const int k1 = __ldg(a.rp + k + 1);
+            for (int q = p + 1; q < q1; ++q) {
+              const int pk = find_col(a.ci, dk + 1, k1, __ldg(a.ci + q));
+              if (pk >= 0) a.fval[q] = __dsub_rn(a.fval[q], __dmul_rn(lik, a.fval[pk]));
+            }
+          }
+          if (a.fval[d] == 0.0) pc_error(h, PCS_ZERO_PIVOT, i, 0.0);
+        } else {
+          // IC(0) row of sign * A (precond.py:222-241)
+          double dsum = 0.0;
+          for (int p = q0; p < d; ++p) {
+            const int j = __ldg(a.ci + p);
+            double s = __dmul_rn(sign, __ldg(a.av + p));
+            const int j0 = __ldg(a.rp + j), dj = a.dpos[j];
+            for (int p2 = q0; p2 < p; ++p2) {
+              const int pj = find_col(a.ci, j0, dj, __ldg(a.ci + p2));
+              if (pj >= 0) s = __dsub_rn(s, __dmul_rn(a.fval[p2], a.fval[pj]));
+            }
+            const double lij = __ddiv_rn(s, a.fval[dj]);
+            a.fval[p] = lij;
+            dsum = __dadd_rn(dsum, __dmul_rn(lij, lij));
+          }
+          const double dd = __dsub_rn(__dmul_rn(sign, __ldg(a.av + d)), dsum);
+          if (!(dd > 0.0)) pc_error(h, PCS_ZERO_PIVOT, i, dd);
+          a.fval[d] = sqrt(dd);
+        }
+      }
+      PC_SYNC();
+    }
+    if (a.kind == PC_ICC0) {  // L^T at the upper positions
+      for (int i = gtid; i < n; i += gthreads) {
+        const int d = a.dpos[i];
+        for (int q = d + 1; q < __ldg(a.rp + i + 1); ++q) {
+          const int j = __ldg(a.ci + q);
+          a.fval[q] = a.fval[find_col(a.ci, __ldg(a.rp + j), a.dpos[j], i)];
+        }
+      }
+    }
+  }
+  if (gtid == 0) {
+    PcView& v = h->v;
+    v.kind = a.kind;
+    v.n = n;
+    v.rp = a.rp;
+    v.ci = a.ci;
+    v.fval = a.fval;
+    v.dpos = a.dpos;
+    for (int q = 0; q < 2; ++q) {
+      v.lptr[q] = a.lptr[q];
+      v.lrows[q] = a.lrows[q];
+    }
+    v.nlev[0] = nlev0;
+    v.nlev[1] = nlev1;
+    v.scale = sign;
+    v.bs = v.nb = 0;
+    v.lu = nullptr;
+    v.perm = nullptr;
+    v.upper[0] = 0;
+    v.upper[1] = 1;
+    if (a.kind == PC_SOR) {
+      v.nsweep = 1;
+      v.dmode[0] = PCD_FACTOR;
+      v.dmode[1] = PCD_UNIT;
+    } else if (a.kind == PC_ILU0) {
+      v.nsweep = 2;
+      v.dmode[0] = PCD_UNIT;
+      v.dmode[1] = PCD_FACTOR;
+    } else {
+      v.nsweep = 2;
+      v.dmode[0] = PCD_FACTOR;
+      v.dmode[1] = PCD_FACTOR;
+    }
+  }
+#undef PC_SYNC
+}
+
+// out[:, c] = M^-1 in[:, c] (in == out allowed), standalone (own barrier words)
+__global__ void __launch_bounds__(NT) k_pc_apply(PcHeader* h, const double* in, double* out,
+                                                 int ncols, size_t ld_in, size_t ld_out) {
+  __shared__ int s_flag;
+  __shared__ PcView s_pc;
+  if (threadIdx.x == 0) s_pc = h->v;
+  __syncthreads();
+  const PcView& pc = s_pc;
+  const int tid = threadIdx.x;
+  unsigned long long seen =
+      tid == 0 ? ld_relaxed_gpu64(&h->bar_count) / (unsigned long long)gridDim.x : 0ull;
+  auto sync = [&]() -> bool { return grid_sync(&h->bar_count, &h->abort_flag, gridDim.x, &s_flag, seen); };
+  if (in != out) {
+    const int gtid = blockIdx.x * NT + tid, gthreads = gridDim.x * NT;
+    for (size_t e = gtid; e < (size_t)pc.n * ncols; e += gthreads)
+      out[(e / pc.n) * ld_out + (e % pc.n)] = in[(e / pc.n) * ld_in + (e % pc.n)];
+    if (!sync()) return;
+  }
+  pc_apply_grid(pc, out, ncols, ld_out, sync);
+}
+
+static int pc_grid(int* out) {
+  static int g_grid[16] = {0};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SKR_ERR_CUDA;
+  if (dev < 0 || dev >= 16) return SKR_ERR_UNSUPPORTED;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!g_grid[dev]) {
+    int sms = 0, nb = 0, nb2 = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pc_build, NT, 0) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_pc_apply, NT, 0) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    // one CTA per SM: every barrier costs with the CTA count, and the sweeps
+    // are latency-bound, not throughput-bound
+    g_grid[dev] = std::max(1, sms * std::min(1, std::min(nb, nb2)));
+  }
+  *out = g_grid[dev];
+  return SKR_OK;
+}
+
+}  // namespace skr
+
+using namespace skr;
+
+extern "C" {
+
+size_t skr_precond_bytes(int32_t kind, int32_t n, int32_t nnz, int32_t block) {
+  if (kind < PC_SOR || kind > PC_BJACOBI || n < 1 || nnz < 0) return 0;
+  if (kind == PC_BJACOBI && (block < 1 || block > 256)) return 0;
+  return pc_layout(kind, n, nnz, block).total;
+}
+
+int skr_precond_build(const skr_csr* A, int32_t kind, double omega, int32_t block, void* buf,
+                      size_t bytes, int32_t* info, double* value, void* stream) {
+  if (!A || !buf || A->n < 1 || !A->row_ptr || !A->col_idx || !A->values) return SKR_ERR_ARG;
+  if (kind < PC_SOR || kind > PC_BJACOBI) return SKR_ERR_ARG;
+  if (kind == PC_SOR && !(omega > 0.0 && omega < 2.0)) return SKR_ERR_ARG;
+  if (kind == PC_BJACOBI && block < 1) return SKR_ERR_ARG;
+  if (kind == PC_BJACOBI && block > 256) return SKR_ERR_UNSUPPORTED;
+  const PcLayout L = pc_layout(kind, A->n, A->nnz, block);
+  if (bytes < L.total) return SKR_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int grid = 0;
+  if (int rc = pc_grid(&grid)) return rc;
+  char* base = (char*)buf;
+  PcHeader hh;
+  memset(&hh, 0, sizeof(hh));
+  hh.err_row = A->n;
+  if (cudaMemcpyAsync(base, &hh, sizeof(hh), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return SKR_ERR_CUDA;
+  PcBuildArgs a{};
+  a.h = (PcHeader*)base;
+  a.kind = kind;
+  a.n = A->n;
+  a.rp = A->row_ptr;
+  a.ci = A->col_idx;
+  a.av = A->values;
+  a.omega = omega;
+  a.fval = (double*)(base + L.fval);
+  a.dpos = (int*)(base + L.dpos);
+  for (int h = 0; h < 2; ++h) {
+    a.lptr[h] = (int*)(base + L.lptr[h]);
+    a.lrows[h] = (int*)(base + L.lrows[h]);
+    a.lev[h] = (int*)(base + L.lev[h]);
+    a.cur[h] = (int*)(base + L.cur[h]);
+  }
+  a.bs = block;
+  a.nb = kind == PC_BJACOBI ? (A->n + block - 1) / block : 0;
+  a.lu = (double*)(base + L.lu);
+  a.perm = (int*)(base + L.perm);
+  void* args[1] = {&a};
+  if (cudaLaunchCooperativeKernel((const void*)k_pc_build, dim3(grid), dim3(NT), args, 0, s) !=
+      cudaSuccess)
+    return SKR_ERR_CUDA;
+  if (info) {
+    // the reference raises from the constructor: report the outcome now
+    if (cudaMemcpyAsync(&hh, base, sizeof(hh), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return SKR_ERR_CUDA;
+    info[0] = hh.status;
+    info[1] = hh.err_row;
+    if (value) *value = hh.err_value;
+    if (hh.status == PCS_ABORTED) return SKR_ERR_TIMEOUT;
+  }
+  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+}
+
+int skr_precond_apply(const void* pc, const double* in, double* out, int32_t ncols, int64_t ld_in,
+                      int64_t ld_out, void* stream) {
+  if (!pc || !in || !out || ncols < 0) return SKR_ERR_ARG;
+  if (ncols == 0) return SKR_OK;
+  int grid = 0;
+  if (int rc = pc_grid(&grid)) return rc;
+  PcHeader* h = (PcHeader*)pc;
+  size_t li = (size_t)ld_in, lo = (size_t)ld_out;
+  int nc = ncols;
+  void* args[6] = {&h, &in, &out, &nc, &li, &lo};
+  if (cudaLaunchCooperativeKernel((const void*)k_pc_apply, dim3(grid), dim3(NT), args, 0,
+                                  (cudaStream_t)stream) != cudaSuccess)
+    return SKR_ERR_CUDA;
+  return SKR_OK;
+}
+
+}  // extern "C"

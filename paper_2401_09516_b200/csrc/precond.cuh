@@ -1,0 +1,203 @@
+// General left preconditioners on the device (kryrec/precond.py:80-145, :251-312):
+// SOR, ILU(0), IC(0) as level-scheduled sparse triangular sweeps, block Jacobi
+// as per-block dense LU solves. "apply" = solve M z = v in place.
+//
+// Triangular kinds keep their factor on the CSR pattern of the matrix they
+// were built from (rows sorted): fval[q] is the factor entry at pattern
+// position q, dpos[i] the position of row i's diagonal. The lower sweep uses
+// the entries left of the diagonal, the upper sweep those right of it (IC(0)
+// stores L^T there, mirrored at build time). Rows are grouped into dependency
+// levels (all rows of a level are independent). A sweep walks the levels;
+// runs of narrow levels are swept by CTA 0 alone with a block barrier per
+// level, wide levels by the whole grid with one grid barrier each. Each row is
+// one sequential sum (separate multiply and subtract), so the result does not
+// depend on how a level's rows are spread over threads.
+#pragma once
+#include "skr_device.cuh"
+
+namespace skr {
+
+enum PcKind { PC_NONE = 0, PC_SOR = 1, PC_ILU0 = 2, PC_ICC0 = 3, PC_BJACOBI = 4 };
+enum PcDiv { PCD_UNIT = 0, PCD_FACTOR = 1 };
+enum PcStatus { PCS_OK = 0, PCS_ZERO_PIVOT = 1, PCS_NOT_SYMMETRIC = 2, PCS_ABORTED = 3 };
+
+constexpr int PC_NARROW = 2 * NT;  // rows up to which a level is swept by one CTA
+
+struct PcView {
+  int kind;        // PcKind
+  int n;
+  int nsweep;      // triangular sweeps per apply (1: SOR, 2: ILU0 / ICC0)
+  int upper[2];    // sweep s uses the upper (1) or lower (0) part
+  int dmode[2];    // PcDiv of sweep s
+  int nlev[2];     // levels of the lower [0] / upper [1] schedule
+  const int* rp;   // pattern the factor lives on (the caller's CSR arrays)
+  const int* ci;
+  const double* fval;
+  const int* dpos;
+  const int* lptr[2];   // level l of schedule h: rows lrows[h][lptr[h][l] .. lptr[h][l+1])
+  const int* lrows[2];
+  double scale;         // ICC0: sign (1 otherwise)
+  int bs, nb;           // block Jacobi: block size, number of blocks
+  const double* lu;     // nb x (bs x bs) column-major LU factors (unit L below the diagonal)
+  const int* perm;      // n: row (within its block) gathered into position i
+};
+
+// Device-resident head of a preconditioner buffer (skr_precond_build).
+struct PcHeader {
+  PcView v;
+  int status;           // PcStatus
+  int err_row;          // first row with a zero / nonpositive pivot (n: none)
+  double err_value;
+  int any_nonneg_diag;  // ICC0 sign test
+  int maxlev[2];
+  int chg[3];
+  int pad0[32];
+  unsigned long long bar_count;  // the build / standalone-apply kernels' grid barrier
+  unsigned bar_pad[62];
+  int abort_flag;
+};
+
+// One triangular sweep over `ncols` columns of v (leading dimension ldv),
+// grid-cooperative: sync() is the caller's grid barrier (false = aborted).
+template <class Sync>
+__device__ __forceinline__ bool pc_tri_sweep(const PcView& pc, int s, double* v, int ncols,
+                                             size_t ldv, Sync&& sync) {
+  const int up = pc.upper[s], dm = pc.dmode[s];
+  const int* lptr = pc.lptr[up];
+  const int* lrows = pc.lrows[up];
+  const int nlev = pc.nlev[up];
+  auto do_rows = [&](int lo, int nr, int first, int stride) {
+    for (int it = first; it < nr * ncols; it += stride) {
+      const int i = __ldg(lrows + lo + it % nr);
+      double* col = v + (size_t)(it / nr) * ldv;
+      const int d = __ldg(pc.dpos + i);
+      const int q0 = up ? d + 1 : __ldg(pc.rp + i), q1 = up ? __ldg(pc.rp + i + 1) : d;
+      double acc = col[i];
+      for (int q = q0; q < q1; ++q)
+        acc = __dsub_rn(acc, __dmul_rn(__ldg(pc.fval + q), col[__ldg(pc.ci + q)]));
+      if (dm == PCD_FACTOR) acc = __ddiv_rn(acc, __ldg(pc.fval + d));
+      col[i] = acc;
+    }
+  };
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gthreads = gridDim.x * blockDim.x;
+  int l = 0;
+  int lo = __ldg(lptr);
+  while (l < nlev) {
+    int hi = __ldg(lptr + l + 1);
+    if ((hi - lo) * ncols <= PC_NARROW) {
+      // a run of narrow levels: CTA 0 alone, a block barrier per level
+      int l1 = l;
+      while (true) {
+        if (blockIdx.x == 0) {
+          do_rows(lo, hi - lo, threadIdx.x, blockDim.x);
+          __syncthreads();
+        }
+        lo = hi;
+        ++l1;
+        if (l1 >= nlev) break;
+        const int h2 = __ldg(lptr + l1 + 1);
+        if ((h2 - lo) * ncols > PC_NARROW) break;
+        hi = h2;
+      }
+      l = l1;
+    } else {
+      do_rows(lo, hi - lo, gtid, gthreads);
+      lo = hi;
+      ++l;
+    }
+    if (!sync()) return false;
+  }
+  return true;
+}
+
+// Block Jacobi: block b's slice of every column <- U^-1 L^-1 P (slice), one
+// warp per (block, column); RB = ceil(bs / 32) entries per lane in registers.
+template <int RB>
+__device__ __forceinline__ void pc_block_solve(const PcView& pc, double* v, int ncols, size_t ldv,
+                                               int n) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int bs = pc.bs;
+  for (int it = gw; it < pc.nb * ncols; it += nw) {
+    const int b = it % pc.nb;
+    double* col = v + (size_t)(it / pc.nb) * ldv;
+    const int start = b * bs, bsz = min(bs, n - start);
+    const double* lu = pc.lu + (size_t)b * bs * bs;
+    double x[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int i = 32 * r + lane;
+      x[r] = i < bsz ? col[start + __ldg(pc.perm + start + i)] : 0.0;
+    }
+    __syncwarp();  // every gather is done before the slice is overwritten
+    // forward, unit lower
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      for (int kl = 0; kl < 32; ++kl) {
+        const int k = 32 * r + kl;
+        if (k >= bsz) break;
+        const double xk = __shfl_sync(0xffffffffu, x[r], kl);
+#pragma unroll
+        for (int r2 = r; r2 < RB; ++r2) {
+          const int i = 32 * r2 + lane;
+          if (i > k && i < bsz)
+            x[r2] = __dsub_rn(x[r2], __dmul_rn(__ldg(lu + i + (size_t)k * bs), xk));
+        }
+      }
+    // backward, upper
+#pragma unroll
+    for (int r = RB - 1; r >= 0; --r)
+      for (int kl = 31; kl >= 0; --kl) {
+        const int k = 32 * r + kl;
+        if (k >= bsz) continue;
+        if (lane == kl) x[r] = __ddiv_rn(x[r], __ldg(lu + k + (size_t)k * bs));
+        const double xk = __shfl_sync(0xffffffffu, x[r], kl);
+#pragma unroll
+        for (int r2 = 0; r2 <= r; ++r2) {
+          const int i = 32 * r2 + lane;
+          if (i < k) x[r2] = __dsub_rn(x[r2], __dmul_rn(__ldg(lu + i + (size_t)k * bs), xk));
+        }
+      }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int i = 32 * r + lane;
+      if (i < bsz) col[start + i] = x[r];
+    }
+  }
+}
+
+// v[:, c] <- M^-1 v[:, c] for c < ncols, by every CTA of a cooperative grid.
+// The caller has made v visible grid-wide (a barrier after it was written);
+// on return (true) the result is visible grid-wide as well.
+template <class Sync>
+__device__ __forceinline__ bool pc_apply_grid(const PcView& pc, double* v, int ncols, size_t ldv,
+                                              Sync&& sync) {
+  const int n = pc.n;
+  if (pc.kind == PC_BJACOBI) {
+    if (pc.bs <= 32)
+      pc_block_solve<1>(pc, v, ncols, ldv, n);
+    else if (pc.bs <= 64)
+      pc_block_solve<2>(pc, v, ncols, ldv, n);
+    else if (pc.bs <= 128)
+      pc_block_solve<4>(pc, v, ncols, ldv, n);
+    else
+      pc_block_solve<8>(pc, v, ncols, ldv, n);
+    return sync();
+  }
+  for (int s = 0; s < pc.nsweep; ++s)
+    if (!pc_tri_sweep(pc, s, v, ncols, ldv, sync)) return false;
+  if (pc.scale != 1.0) {
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gthreads = gridDim.x * blockDim.x;
+    for (size_t e = gtid; e < (size_t)n * ncols; e += gthreads) {
+      double* q = v + (e / n) * ldv + (e % n);
+      *q = __dmul_rn(pc.scale, *q);
+    }
+    return sync();
+  }
+  return true;
+}
+
+}  // namespace skr

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .gmres import SolveReport, SolverConfig
-from .precond import JacobiPreconditioner, Preconditioner
+from .precond import DevicePreconditioner, JacobiPreconditioner, Preconditioner
 from .sparse import CsrMatrix, DeviceCsr
 
 __all__ = ["RecycleSpace", "GcroDrEngine", "gcrodr_solve", "harmonic_ritz_first_cycle",
@@ -206,7 +206,8 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
 
     Returns ``(SolveReport, RecycleSpace)``. ``A`` may be a host CSR
     (this package's or kryrec's ``CsrMatrix``) or a ``DeviceCsr``; ``M`` is
-    None / IdentityPreconditioner / JacobiPreconditioner. The recycle pair
+    None or any preconditioner of ``build_preconditioner`` (none, jacobi,
+    bjacobi, sor, ilu0, icc0). The recycle pair
     comes back as CUDA tensors and can be passed straight to the next call.
     """
     import torch
@@ -215,10 +216,15 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
     t0 = time.perf_counter()
     _lib.require_cuda()
     jacobi = isinstance(M, JacobiPreconditioner) or getattr(M, "kind", "none") == "jacobi"
-    if M is not None and not jacobi and getattr(M, "kind", "none") != "none":
-        raise NotImplementedError(f"preconditioner {M.kind!r} is not on the device path")
+    general = M if isinstance(M, DevicePreconditioner) else None
+    if M is not None and not jacobi and general is None and getattr(M, "kind", "none") != "none":
+        raise NotImplementedError(
+            f"preconditioner {M.kind!r}: build it with this package's build_preconditioner "
+            "(the factorization lives on the device)")
     if isinstance(A, DeviceCsr):
         dA = A
+        if general is None and dA.precond is not None:
+            dA = dA.with_precond(None)
         if jacobi and dA.diag is None:
             dA = dA.with_diag(M.device_diag() if isinstance(M, JacobiPreconditioner)
                               else None)
@@ -233,6 +239,8 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
             diag = (M.device_diag() if isinstance(M, JacobiPreconditioner)
                     else torch.from_numpy(host.diagonal()).to("cuda"))
             dA = dA.with_diag(diag)
+    if general is not None:
+        dA = dA.with_precond(general)
     n = dA.n
     bt = _to_device_vec(b, n, "right-hand side")
     x0t = _to_device_vec(x0, n, "x0") if x0 is not None else None

@@ -26,6 +26,7 @@ import numpy as np
 from . import _lib
 from .gcrodr import engine_for
 from .gmres import SolverConfig
+from .precond import DEVICE_KINDS, KINDS, build_device_preconditioner
 from .sparse import DeviceCsr
 
 __all__ = ["SequenceResult", "ChainState", "solve_sequence", "solve_chains", "chunk_positions",
@@ -77,19 +78,32 @@ def _nbytes(t) -> int:
     return int(t.numel() * t.element_size())
 
 
-def _upload(sysobj, jacobi: bool, stream):
+def _with_general(dA, precond: str, stream, opts):
+    """Attach the device-built preconditioner of kind ``precond`` (bjacobi, sor,
+    ilu0, icc0; precond.py:251-312) unless the matrix already carries one."""
+    if precond in DEVICE_KINDS and dA.precond is None:
+        dA = dA.with_precond(build_device_preconditioner(dA, precond, stream=stream,
+                                                         **(opts or {})))
+    return dA
+
+
+def _upload(sysobj, precond, stream, opts=None):
     """Host system -> (DeviceCsr, b_dev, bytes). Accepts (A, b) pairs where the
     arrays are numpy or (ideally pinned) torch CPU tensors, or a DeviceCsr."""
     import torch
 
     A, b = sysobj
+    jacobi = precond == "jacobi"
     if isinstance(A, DeviceCsr):
         bt = b if isinstance(b, torch.Tensor) and b.is_cuda else torch.as_tensor(b).to("cuda")
+        with torch.cuda.stream(stream):
+            A = _with_general(A, precond, stream, opts)
         return A, bt, 0
     with torch.cuda.stream(stream):
         # the zero-pivot check is deferred (no sync on the upload stream)
         dA = DeviceCsr.from_host(A, jacobi=jacobi, non_blocking=True, stream=stream,
                                  check_pivot=False)
+        dA = _with_general(dA, precond, stream, opts)
         if isinstance(b, torch.Tensor):
             bt = b.to("cuda", dtype=torch.float64, non_blocking=True)
         else:
@@ -102,7 +116,8 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
                    cfg: SolverConfig, precond: str = "none", *, positions: Sequence[int] = None,
                    keep_x: str = "host", stream=None, recycle_first=None,
                    want_history: bool = False, chain: ChainState = None,
-                   engine_slot: int = 0, grid_ctas: int = 0) -> SequenceResult:
+                   engine_slot: int = 0, grid_ctas: int = 0,
+                   precond_opts: dict = None) -> SequenceResult:
     """Solve ``systems[order[p]]`` for p in ``positions`` (default: all) as one
     recycling chain. ``systems`` is a sequence of (A, b) or a callable idx ->
     (A, b) (lazy generation for large configs). ``keep_x``: "host" (x copied
@@ -111,9 +126,8 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
     import torch
 
     _lib.require_cuda()
-    if precond not in ("none", "jacobi"):
-        raise NotImplementedError(f"preconditioner {precond!r} is not on the device path")
-    jacobi = precond == "jacobi"
+    if precond not in KINDS:
+        raise ValueError(f"unknown preconditioner kind {precond!r}; expected one of {KINDS}")
     positions = list(range(len(order))) if positions is None else list(positions)
     get = systems if callable(systems) else (lambda i: systems[i])
     res = SequenceResult(order=[int(order[p]) for p in positions])
@@ -123,7 +137,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
     side = torch.cuda.Stream()
     t0 = time.perf_counter()
     # first upload
-    nxt = _upload(get(res.order[0]), jacobi, side)
+    nxt = _upload(get(res.order[0]), precond, side, precond_opts)
     ev = torch.cuda.Event()
     ev.record(side)
     eng = None
@@ -145,7 +159,7 @@ def solve_sequence(systems: Sequence | Callable[[int], tuple], order: Sequence[i
             eng = engine_for(dA.n, cfg, slot=engine_slot, grid_ctas=grid_ctas)
         # prefetch the next system while this one solves
         if i + 1 < len(res.order):
-            nxt = _upload(get(res.order[i + 1]), jacobi, side)
+            nxt = _upload(get(res.order[i + 1]), precond, side, precond_opts)
             ev = torch.cuda.Event()
             ev.record(side)
         x = torch.empty(dA.n, dtype=torch.float64, device="cuda")
@@ -266,8 +280,8 @@ def _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states, g
     t_enter = time.perf_counter()
     get = systems if callable(systems) else (lambda i: systems[i])
     jacobi = precond == "jacobi"
-    if precond not in ("none", "jacobi"):
-        raise NotImplementedError(f"preconditioner {precond!r} is not on the device path")
+    if precond not in KINDS:
+        raise ValueError(f"unknown preconditioner kind {precond!r}; expected one of {KINDS}")
     sysl, firsts, idxs = [], [0], []
     for ch in chunks:
         for pos in ch:
@@ -276,6 +290,7 @@ def _solve_chains_native(systems, order, cfg, precond, chunks, keep_x, states, g
                 return None
             if jacobi and A.c.diag is None:
                 return None
+            A = _with_general(A, precond, None, None)
             sysl.append((A, b))
             idxs.append(int(order[pos]))
         firsts.append(len(sysl))

@@ -141,7 +141,8 @@ class DeviceCsr:
     only if the device check found the matrix to be a symmetric 7-diagonal
     one, with bit-identical results)."""
 
-    def __init__(self, n, row_ptr, col_idx, values, diag=None, keep=None, stencil=None):
+    def __init__(self, n, row_ptr, col_idx, values, diag=None, keep=None, stencil=None,
+                 precond=None):
         self.n = int(n)
         self.row_ptr = row_ptr
         self.col_idx = col_idx
@@ -149,11 +150,15 @@ class DeviceCsr:
         self.diag = diag
         self._keep = keep
         self.stencil = stencil  # (device buffer, sx, sxy) or None
+        # general preconditioner: an object with .buffer (device bytes built by
+        # skr_precond_build; it keeps the pattern it was built on alive) or None
+        self.precond = precond
         buf, sx, sxy = stencil if stencil is not None else (None, 0, 0)
         self.c = _lib.SkrCsr(self.n, int(values.numel()), row_ptr.data_ptr(),
                              col_idx.data_ptr(), values.data_ptr(),
                              diag.data_ptr() if diag is not None else None,
-                             buf.data_ptr() if buf is not None else None, int(sx), int(sxy))
+                             buf.data_ptr() if buf is not None else None, int(sx), int(sxy),
+                             precond.buffer.data_ptr() if precond is not None else None)
 
     def stencil_active(self) -> bool:
         """True when the device check accepted the stencil form (syncs)."""
@@ -172,11 +177,12 @@ class DeviceCsr:
             return self
         buf = torch.empty(nbytes, dtype=torch.uint8, device=self.values.device)
         probe = _lib.SkrCsr(self.n, int(self.values.numel()), self.row_ptr.data_ptr(),
-                            self.col_idx.data_ptr(), self.values.data_ptr(), None, None, 0, 0)
+                            self.col_idx.data_ptr(), self.values.data_ptr(), None, None, 0, 0,
+                            None)
         _lib.check(L.skr_stencil_build(ctypes.byref(probe), sx, sxy, buf.data_ptr(), nbytes,
                                        _lib.stream_handle(stream)), "skr_stencil_build")
         return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, self.diag, self._keep,
-                         (buf, sx, sxy))
+                         (buf, sx, sxy), self.precond)
 
     @property
     def nnz(self) -> int:
@@ -241,7 +247,16 @@ class DeviceCsr:
 
     def with_diag(self, diag):
         return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, diag, self._keep,
-                         self.stencil)
+                         self.stencil, self.precond)
+
+    def with_precond(self, precond):
+        """The same matrix with a general preconditioner (precond.DevicePreconditioner
+        or None) attached; it replaces the Jacobi diagonal in every kernel."""
+        if precond is not None and precond.n != self.n:
+            raise ValueError(f"preconditioner size {precond.n} does not match {self.n} rows")
+        return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values,
+                         None if precond is not None else self.diag, self._keep, self.stencil,
+                         precond)
 
 
 class _nullctx:

@@ -102,8 +102,10 @@ def test_solver_config_and_csr_validation():
         skr.ParameterMatrix(np.array([np.inf]))
     with pytest.raises(skr.ZeroPivotError):
         skr.build_preconditioner(skr.CsrMatrix(2, 2, [0, 1, 2], [1, 0], [1.0, 1.0]), "jacobi")
-    with pytest.raises(NotImplementedError):
-        skr.build_preconditioner(skr.eye(2), "ilu0")
+    if not __import__("torch").cuda.is_available():
+        # the factorization lives on the device: no CPU fallback
+        with pytest.raises(skr._lib.SkrExtensionError):
+            skr.build_preconditioner(skr.eye(2), "ilu0")
     with pytest.raises(ValueError):
         skr.build_preconditioner(skr.eye(2), "bogus")
     assert skr.build_preconditioner(skr.eye(3), "none").kind == "none"

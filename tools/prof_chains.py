@@ -36,7 +36,7 @@ ncyc = max(1, tot[9])
 for i, nm in enumerate(names):
     print(f"  all chains {nm:13s} {tot[16 + i] / its / 1.9e3:8.2f} us/iteration")
 for i, nm in ((7, "last sweep2+y"), (8, "x update+Gram"), (9, "barrier x"), (10, "resid"),
-              (11, "barrier"), (5, "reduce tail")):
+              (11, "barrier"), (5, "reduce tail"), (12, "START update"), (13, "START V0+sync")):
     idx = 16 + i if i != 5 else 21
     print(f"  all chains cycle end {nm:14s} {tot[idx] / ncyc / 1.9e3:8.2f} us/cycle")
 print("  dense calls", int(tot[9]), "sweeps", int(tot[22]))

@@ -39,6 +39,6 @@ for i, nm in enumerate(["sweep1", "barrier(red)", "LS+control", "sweep2", "barri
     print(f"  cycle {nm:13s} {prof[16 + i] / its / 1.9e3:8.2f} us/iteration")
 ncyc = max(1, prof[9])
 for i, nm in ((7, "last sweep2+y"), (8, "x update"), (9, "barrier x"), (10, "resid+Gram"),
-              (11, "barrier Gram"), (5, "reduce tail")):
+              (11, "barrier Gram"), (5, "reduce tail"), (12, "START update"), (13, "START V0+sync")):
     idx = 16 + i if i != 5 else 21
     print(f"  cycle end {nm:14s} {prof[idx] / ncyc / 1.9e3:8.2f} us/cycle")

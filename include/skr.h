@@ -259,6 +259,15 @@ int skr_sort_dist2(const double* params, int32_t n_sys, int64_t P, int32_t row0,
                    size_t ws_bytes, void* stream);
 int skr_sort_chain(const double* D2, const double* params, int32_t n_sys, int64_t P,
                    int32_t exact_d2, int32_t* order, int32_t* n_certified, void* stream);
+/* grouped_sort's bucketing key (sorting.py:96-105: the first principal
+ * coordinate of the centered batch, sign rule included) from the full D2
+ * matrix: the dominant eigenpair of the double-centered G = -1/2 J D2 J by
+ * trace-normalised repeated squaring + power refinement (no SVD). keys:
+ * n_sys doubles (device) = sqrt(lambda_1) u_1, the reference's centered @ vt[0]
+ * up to rounding. Stream-ordered. */
+size_t skr_sort_pca_workspace_bytes(int32_t n_sys);
+int skr_sort_pca_keys(const double* D2, const double* params, int32_t n_sys, int64_t P,
+                      double* keys, void* workspace, size_t ws_bytes, void* stream);
 /* one-call single-GPU greedy_sort (sorting.py:72-80) */
 int skr_greedy_sort(const double* params, int32_t n_sys, int64_t P, int32_t* order_host,
                     void* workspace, size_t ws_bytes, void* stream);

@@ -25,6 +25,7 @@ EXPORTS = (
     "skr_sort_workspace_bytes", "skr_sort_binary_check", "skr_sort_dist2", "skr_sort_chain",
     "skr_greedy_sort", "skr_dense_hr_first", "skr_dense_hr_next",
     "skr_precond_bytes", "skr_precond_build", "skr_precond_apply",
+    "skr_sort_pca_workspace_bytes", "skr_sort_pca_keys",
 )
 
 
@@ -118,6 +119,8 @@ def _declare(L):
                                c_int32),
         "skr_dense_hr_next": ([P, c_int32, P, c_int32, c_int32, c_int32, P, c_int32,
                                POINTER(c_int32), P], c_int32),
+        "skr_sort_pca_workspace_bytes": ([c_int32], c_size_t),
+        "skr_sort_pca_keys": ([P, P, c_int32, c_int64, P, P, c_size_t, P], c_int32),
         "skr_precond_bytes": ([c_int32, c_int32, c_int32, c_int32], c_size_t),
         "skr_precond_build": ([POINTER(SkrCsr), c_int32, c_double, c_int32, P, c_size_t,
                                POINTER(c_int32), POINTER(c_double), P], c_int32),

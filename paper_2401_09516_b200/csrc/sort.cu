@@ -399,6 +399,250 @@ static SortLayout sort_layout(int n_sys, int64_t P) {
   return L;
 }
 
+
+// ---------------------------------------------------------------------------
+// grouped_sort's first principal coordinate (sorting.py:96-105) without the
+// SVD of the centered batch: the Gram matrix of the centered rows is the
+// double-centered distance matrix, G = -1/2 J D2 J (J = I - 11^T / n), and the
+// reference's key = centered @ vt[0] is sqrt(lambda_1) u_1 for G's dominant
+// eigenpair. u_1 comes from PCA_SQUARINGS trace-normalised squarings of G
+// (G^(2^s) -> u u^T; own fp64 GEMM tiles) and PCA_REFINE power steps on G
+// itself; the sign follows the reference's rule on vt[0] = flat^T u / |.|
+// (largest-magnitude component positive, first index on ties).
+// ---------------------------------------------------------------------------
+constexpr int PCA_SQUARINGS = 24;
+constexpr int PCA_REFINE = 6;
+constexpr int PT = 64;  // GEMM tile
+
+__global__ void __launch_bounds__(256) k_pca_rowmean(const double* __restrict__ D2, int n,
+                                                     double* rm) {
+  // rm[i] = mean_j D2[i][j]; one warp per row, fixed order
+  const int lane = threadIdx.x & 31, w = (blockIdx.x * 256 + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * 256) >> 5;
+  for (int i = w; i < n; i += nw) {
+    double sacc = 0.0;
+    for (int j = lane; j < n; j += 32) sacc += D2[(size_t)i * n + j];
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) rm[i] = sacc / n;
+  }
+}
+__global__ void __launch_bounds__(1024) k_pca_mean(const double* rm, int n, double* mu) {
+  __shared__ double sh[1024];
+  double sacc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) sacc += rm[i];
+  sh[threadIdx.x] = sacc;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mu[0] = sh[0] / n;
+    mu[1] = 1.0;  // scale of the first squaring
+  }
+}
+__global__ void __launch_bounds__(256) k_pca_center(const double* __restrict__ D2, int n,
+                                                    const double* rm, const double* mu,
+                                                    double* G) {
+  const size_t tot = (size_t)n * n;
+  for (size_t e = (size_t)blockIdx.x * 256 + threadIdx.x; e < tot; e += (size_t)gridDim.x * 256) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    // symmetric by construction: the two row means enter in a fixed order
+    const double a = i <= j ? rm[i] : rm[j], b = i <= j ? rm[j] : rm[i];
+    const double d = i <= j ? D2[e] : D2[(size_t)j * n + i];
+    G[e] = -0.5 * (((d - a) - b) + mu[0]);
+  }
+}
+// C = (B^T B) / t^2 for symmetric B (row-major n x n), t = *scale (the trace
+// of B as the previous squaring left it unnormalised); 64 x 64 tiles, 4 x 4 per thread
+__global__ void __launch_bounds__(256) k_pca_square(const double* __restrict__ B, int n,
+                                                    const double* scale, double* C) {
+  __shared__ double sa[16][PT + 1], sb[16][PT + 1];
+  const int i0 = blockIdx.y * PT, j0 = blockIdx.x * PT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < n; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * PT; e += 256) {
+      const int kk = e / PT, c = e % PT, k = k0 + kk;
+      sa[kk][c] = (k < n && i0 + c < n) ? B[(size_t)k * n + i0 + c] : 0.0;
+      sb[kk][c] = (k < n && j0 + c < n) ? B[(size_t)k * n + j0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = sa[kk][ty + 16 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = sb[kk][tx + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+  const double t = *scale, inv = 1.0 / (t * t);
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = i0 + ty + 16 * x, j = j0 + tx + 16 * y;
+      if (i < n && j < n) C[(size_t)i * n + j] = acc[x][y] * inv;
+    }
+}
+__global__ void __launch_bounds__(1024) k_pca_trace(const double* C, int n, double* scale) {
+  __shared__ double sh[1024];
+  double sacc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) sacc += C[(size_t)i * n + i];
+  sh[threadIdx.x] = sacc;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) scale[0] = sh[0] > 0.0 ? sh[0] : 1.0;
+}
+// one CTA: u = normalised row argmax diag(C) of C ~ u u^T, then power steps on G
+__global__ void __launch_bounds__(1024) k_pca_finish(const double* C, const double* G, int n,
+                                                     double* u, double* w, double* lam) {
+  __shared__ double sh[1024];
+  __shared__ int si[1024];
+  const int tid = threadIdx.x;
+  double best = -1.0;
+  int bi = n;
+  for (int i = tid; i < n; i += 1024) {
+    const double d = C[(size_t)i * n + i];
+    if (d > best) {
+      best = d;
+      bi = i;
+    }
+  }
+  sh[tid] = best;
+  si[tid] = bi;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o && (sh[tid + o] > sh[tid] || (sh[tid + o] == sh[tid] && si[tid + o] < si[tid]))) {
+      sh[tid] = sh[tid + o];
+      si[tid] = si[tid + o];
+    }
+    __syncthreads();
+  }
+  const int js = si[0] < n ? si[0] : 0;
+  __syncthreads();
+  auto normalise = [&](const double* src, double* dst) -> double {  // returns |src|
+    double q = 0.0;
+    for (int i = tid; i < n; i += 1024) q += src[i] * src[i];
+    sh[tid] = q;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+      if (tid < o) sh[tid] += sh[tid + o];
+      __syncthreads();
+    }
+    const double nrm = sqrt(sh[0]);
+    __syncthreads();
+    for (int i = tid; i < n; i += 1024) dst[i] = nrm > 0.0 ? src[i] / nrm : src[i];
+    __syncthreads();
+    return nrm;
+  };
+  normalise(C + (size_t)js * n, u);
+  double l = 0.0;
+  for (int it = 0; it < PCA_REFINE; ++it) {
+    // w = G u through G's columns (G symmetric): coalesced over i
+    for (int i = tid; i < n; i += 1024) {
+      double q = 0.0;
+      for (int j = 0; j < n; ++j) q = fma(G[(size_t)j * n + i], u[j], q);
+      w[i] = q;
+    }
+    __syncthreads();
+    l = normalise(w, u);  // |G u| -> lambda_1 for a unit u
+  }
+  if (tid == 0) lam[0] = l;
+}
+// d_j = sum_i u_i flat[i][j] (= (centered^T u)_j: sum_i u_i = 0); per-CTA
+// arg max |d_j| (first index on ties) -> part[3 b .. 3 b + 2] = |d|, j, d
+__global__ void __launch_bounds__(256) k_pca_dir(const double* __restrict__ flat, int n, int64_t P,
+                                                 const double* __restrict__ u, double* part) {
+  __shared__ double sv[256], sd[256];
+  __shared__ long long sj[256];
+  double best = -1.0, bd = 0.0;
+  long long bj = P;
+  for (int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x; j < P; j += (int64_t)gridDim.x * 256) {
+    double d = 0.0;
+    for (int i = 0; i < n; ++i) d = fma(__ldg(u + i), flat[(size_t)i * P + j], d);
+    if (fabs(d) > best) {
+      best = fabs(d);
+      bj = j;
+      bd = d;
+    }
+  }
+  sv[threadIdx.x] = best;
+  sj[threadIdx.x] = bj;
+  sd[threadIdx.x] = bd;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    const int t = threadIdx.x;
+    if (t < o && (sv[t + o] > sv[t] || (sv[t + o] == sv[t] && sj[t + o] < sj[t]))) {
+      sv[t] = sv[t + o];
+      sj[t] = sj[t + o];
+      sd[t] = sd[t + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = sv[0];
+    part[3 * blockIdx.x + 1] = (double)sj[0];
+    part[3 * blockIdx.x + 2] = sd[0];
+  }
+}
+__global__ void __launch_bounds__(256) k_pca_keys(const double* part, int nb, const double* u,
+                                                  const double* lam, int n, double* keys) {
+  __shared__ double s_sign;
+  if (threadIdx.x == 0) {
+    double best = -1.0, bj = 0.0, bd = 1.0;
+    for (int b = 0; b < nb; ++b)
+      if (part[3 * b] > best || (part[3 * b] == best && part[3 * b + 1] < bj)) {
+        best = part[3 * b];
+        bj = part[3 * b + 1];
+        bd = part[3 * b + 2];
+      }
+    s_sign = bd < 0.0 ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  const double sc = s_sign * sqrt(fmax(lam[0], 0.0));
+  for (int i = threadIdx.x; i < n; i += 256) keys[i] = sc * u[i];
+}
+
+struct PcaLayout {
+  size_t G, B0, B1, rm, mu, u, w, lam, part, total;
+};
+static PcaLayout pca_layout(int n) {
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  PcaLayout L;
+  size_t off = 0;
+  const size_t nn = (size_t)n * n * sizeof(double);
+  L.G = off;
+  off = al(off + nn);
+  L.B0 = off;
+  off = al(off + nn);
+  L.B1 = off;
+  off = al(off + nn);
+  L.rm = off;
+  off = al(off + (size_t)n * sizeof(double));
+  L.mu = off;
+  off = al(off + 4 * sizeof(double));
+  L.u = off;
+  off = al(off + (size_t)n * sizeof(double));
+  L.w = off;
+  off = al(off + (size_t)n * sizeof(double));
+  L.lam = off;
+  off = al(off + 2 * sizeof(double));
+  L.part = off;
+  off = al(off + 3 * 1184 * sizeof(double));
+  L.total = off;
+  return L;
+}
+
 }  // namespace skrsort
 
 using namespace skrsort;
@@ -472,6 +716,48 @@ int skr_sort_chain(const double* D2, const double* params, int32_t n_sys, int64_
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_chain<<<1, CHAIN_NT, smem, s>>>(D2, params, n_sys, P, exact_d2, order, n_certified);
+  return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
+}
+
+
+size_t skr_sort_pca_workspace_bytes(int32_t n_sys) {
+  if (n_sys <= 0) return 0;
+  return pca_layout(n_sys).total;
+}
+
+int skr_sort_pca_keys(const double* D2, const double* params, int32_t n_sys, int64_t P,
+                      double* keys, void* ws, size_t ws_bytes, void* stream) {
+  if (!D2 || !params || !keys || !ws || n_sys < 2 || P <= 0) return SKR_ERR_ARG;
+  const PcaLayout L = pca_layout(n_sys);
+  if (ws_bytes < L.total) return SKR_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* base = (char*)ws;
+  double* G = (double*)(base + L.G);
+  double* Bb[2] = {(double*)(base + L.B0), (double*)(base + L.B1)};
+  double* rm = (double*)(base + L.rm);
+  double* mu = (double*)(base + L.mu);  // [0] mean of D2, [1] scale of the next squaring
+  double* u = (double*)(base + L.u);
+  double* w = (double*)(base + L.w);
+  double* lam = (double*)(base + L.lam);
+  double* part = (double*)(base + L.part);
+  const int n = n_sys;
+  const int g1 = std::min(1184, (n + 7) / 8);
+  k_pca_rowmean<<<g1, 256, 0, s>>>(D2, n, rm);
+  k_pca_mean<<<1, 1024, 0, s>>>(rm, n, mu);
+  const int g2 = (int)std::min<size_t>(1184 * 4, ((size_t)n * n + 255) / 256);
+  k_pca_center<<<g2, 256, 0, s>>>(D2, n, rm, mu, G);
+  dim3 gg((n + PT - 1) / PT, (n + PT - 1) / PT);
+  const double* src = G;
+  for (int q = 0; q < PCA_SQUARINGS; ++q) {
+    double* dst = Bb[q & 1];
+    k_pca_square<<<gg, 256, 0, s>>>(src, n, mu + 1, dst);
+    k_pca_trace<<<1, 1024, 0, s>>>(dst, n, mu + 1);
+    src = dst;
+  }
+  k_pca_finish<<<1, 1024, 0, s>>>(src, G, n, u, w, lam);
+  const int nb = (int)std::min<int64_t>(1184, (P + 255) / 256);
+  k_pca_dir<<<nb, 256, 0, s>>>(params, n, P, u, part);
+  k_pca_keys<<<1, 256, 0, s>>>(part, nb, u, lam, n, keys);
   return cudaGetLastError() == cudaSuccess ? SKR_OK : SKR_ERR_CUDA;
 }
 

@@ -102,15 +102,39 @@ def greedy_sort(params: Sequence[ParameterMatrix]) -> list[int]:
     return greedy_sort_device(torch.from_numpy(flat).to("cuda"))
 
 
+def principal_keys_device(flat_dev, stream=None):
+    """The first principal coordinate of every row of a (n_sys, P) float64 CUDA
+    tensor (sorting.py:96-105: ``centered @ vt[0]`` with the reference's sign
+    rule), as a CUDA tensor of n_sys keys. Own kernels only: the distance tiles
+    of the sort (skr_sort_dist2), then the dominant eigenpair of the
+    double-centered distance matrix (skr_sort_pca_keys)."""
+    import torch
+
+    n, P = flat_dev.shape
+    flat_dev = flat_dev.contiguous()
+    k = _DeviceSortKernels(stream)
+    k.prepare(flat_dev)
+    D2 = k.dist2_rows(flat_dev, 0, n)
+    L = _lib.load()
+    need = int(L.skr_sort_pca_workspace_bytes(int(n)))
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    keys = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.check(L.skr_sort_pca_keys(D2.data_ptr(), flat_dev.data_ptr(), int(n), int(P),
+                                   keys.data_ptr(), ws.data_ptr(), need,
+                                   _lib.stream_handle(stream)), "skr_sort_pca_keys")
+    return keys
+
+
 def grouped_sort_device(flat_dev, group_size: int, stream=None) -> list[int]:
     """``grouped_sort`` of the rows of a (n_sys, P) float64 CUDA tensor.
 
-    The principal direction (sorting.py:99-101) is the top eigenvector of the
-    smaller Gram matrix of the centered batch (cuBLAS DGEMM + cuSOLVER eigh
-    through torch: O(n_sys^2 P) once); the sign rule, the stable key order and
-    the contiguous groups follow sorting.py:102-110, and every group's chain
-    runs in the device greedy-sort kernels (rows gathered in ascending original
-    index, so the lowest-index tie-break is the reference's)."""
+    The bucketing key (sorting.py:96-105) comes from ``principal_keys_device``
+    (the dominant eigenvector of the batch's double-centered distance matrix,
+    computed by this package's own kernels; the reference takes an SVD of the
+    centered batch: equal up to rounding); the stable key order and the
+    contiguous groups follow sorting.py:105-110, and every group's chain runs in
+    the device greedy-sort kernels (rows gathered in ascending original index,
+    so the lowest-index tie-break is the reference's)."""
     import torch
 
     if group_size < 2:
@@ -118,26 +142,14 @@ def grouped_sort_device(flat_dev, group_size: int, stream=None) -> list[int]:
     n, P = flat_dev.shape
     if n <= group_size:
         return greedy_sort_device(flat_dev, stream)
-    C = flat_dev - flat_dev.mean(dim=0, keepdim=True)
-    if P <= n:
-        _, V = torch.linalg.eigh(C.T @ C)
-        d = V[:, -1]
-    else:
-        _, U = torch.linalg.eigh(C @ C.T)
-        d = C.T @ U[:, -1]
-        nrm = torch.linalg.norm(d)
-        d = d / nrm if float(nrm) > 0 else d
-    lead = int(torch.argmax(d.abs()))
-    if float(d[lead]) < 0:
-        d = -d
-    key = C @ d
-    by_key = torch.argsort(key, stable=True)
+    key = principal_keys_device(flat_dev, stream).cpu().numpy()
+    by_key = np.argsort(key, kind="stable")  # n_sys numbers: host control flow
     order: list[int] = []
     for start in range(0, n, group_size):
-        g = torch.sort(by_key[start:start + group_size]).values
-        sub = greedy_sort_device(flat_dev.index_select(0, g), stream)
-        gl = g.cpu().tolist()
-        order.extend(int(gl[i]) for i in sub)
+        g = np.sort(by_key[start:start + group_size])
+        gd = torch.from_numpy(g).to(flat_dev.device)
+        sub = greedy_sort_device(flat_dev.index_select(0, gd), stream)
+        order.extend(int(g[i]) for i in sub)
     return order
 
 

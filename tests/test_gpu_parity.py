@@ -243,6 +243,32 @@ def test_grouped_sort_golden():
         skr.grouped_sort(dup, 1)
 
 
+def test_principal_keys_match_svd():
+    """The bucketing key of grouped_sort from the package's own kernels (double-
+    centered distance matrix, repeated squaring) against the reference's SVD
+    formula (sorting.py:96-105), on continuous, binary and duplicated batches."""
+    skr = _skr()
+    from paper_2401_09516_b200 import problems as P
+    from paper_2401_09516_b200.sorting import principal_keys_device
+
+    g = np.load(os.path.join(GOLD, "grouped.npz"))
+    batches = [np.stack([P.system_params(spec, i)["params"] for i in range(ns)])
+               for spec, ns in ((P.CONFIGS[1].reduced(n=32), 200), (P.CONFIGS[2].reduced(n=16), 96),
+                                (P.CONFIGS[4].reduced(n=24), 300))] + [np.asarray(g["dup_flat"])]
+    for flat in batches:
+        centered = flat - flat.mean(axis=0)
+        _, sv, vt = np.linalg.svd(centered, full_matrices=False)
+        d = vt[0]
+        if d[np.argmax(np.abs(d))] < 0:
+            d = -d
+        key_ref = centered @ d
+        key = principal_keys_device(torch.from_numpy(flat).cuda()).cpu().numpy()
+        gap = sv[1] / sv[0]
+        err = np.abs(key - key_ref).max() / np.abs(key_ref).max()
+        print("principal keys: n", flat.shape, "sigma2/sigma1 %.4f" % gap, "err %.2e" % err)
+        assert err < 1e-8, (flat.shape, gap, err)
+
+
 def test_sort_ties_and_scalars():
     skr = _skr()
     g = np.load(os.path.join(GOLD, "sort.npz"))

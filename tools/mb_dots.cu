@@ -3,6 +3,7 @@
 // CTA's row slice, at C3 size (N = 2^21), persistent grid of 2 CTAs / SM.
 //   v0: streaming ceiling (every element loaded once, summed per lane)
 //   v1: the k_cycle scheme (64-row warp tiles, 8-column batches, butterfly)
+//   v3: TMA (cp.async.bulk) ring, 2 stages x 32 KB, 2 CTAs / SM; v4: 6 stages, 1 CTA / SM
 //   v2: DMMA m8n8k4 (rows = k; [w z] as the A operand, 8-column groups as B;
 //       accumulators stay in registers for the whole sweep, no butterfly)
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb_dots tools/mb_dots.cu
@@ -169,6 +170,137 @@ __global__ void __launch_bounds__(NT, 2) v2(const double* Q, int ld, int P, cons
   }
 }
 
+
+// v3: CTA-level TMA ring. One producer thread issues 1-D bulk copies
+// (cp.async.bulk, 4 KB = 512 rows of one column) into a ring of STAGES stages
+// of [CBS columns x 512 rows]; the 8 consumer warps each take 64 rows of a
+// stage (same butterfly as v1) and release it through an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}" ::"r"(smem_u32(b)),
+      "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+
+template <int STAGES, int CBS>
+__global__ void __launch_bounds__(NT + 32, 2) v3(const double* Q, int ld, int P, const double* w,
+                                                const double* z, int rpb, int n, double* out) {
+  constexpr int TRC = 512;  // rows per stage (8 warps x 64)
+  extern __shared__ __align__(128) double dsm[];
+  double* ring = dsm;                                  // STAGES x CBS x TRC
+  double* wz = dsm + (size_t)STAGES * CBS * TRC;       // 2 x 2 x TRC (w, z; double-buffered)
+  __shared__ double sacc[NW][2 * 64];
+  __shared__ unsigned long long full[STAGES], empty[STAGES], wzfull[2], wzempty[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
+  const int nrb = (r1 - r0 + TRC - 1) / TRC;           // row blocks (rpb is a multiple of 64;
+  const int ncb = (P + CBS - 1) / CBS;                 //  the last block may be short)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&wzfull[s], 1);
+      mbar_init(&wzempty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp < NW)
+    for (int c = lane; c < 2 * 64; c += 32) sacc[warp][c] = 0.0;
+  __syncthreads();
+  if (warp == NW) {  // producer warp: one thread
+    if (lane == 0) {
+      int it = 0;
+      for (int rb = 0; rb < nrb; ++rb) {
+        const int row0 = r0 + rb * TRC;
+        const int rows = min(TRC, r1 - row0);
+        const unsigned cb = rows * 8;
+        {
+          const int s = rb & 1, ph = (rb >> 1) & 1;
+          if (rb >= 2) mbar_wait(&wzempty[s], ph ^ 1);
+          mbar_expect_tx(&wzfull[s], 2 * cb);
+          bulk_g2s(wz + (size_t)s * 2 * TRC, w + row0, cb, &wzfull[s]);
+          bulk_g2s(wz + (size_t)s * 2 * TRC + TRC, z + row0, cb, &wzfull[s]);
+        }
+        for (int b = 0; b < ncb; ++b, ++it) {
+          const int s = it % STAGES, ph = (it / STAGES) & 1;
+          if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+          const int nc = min(CBS, P - b * CBS);
+          mbar_expect_tx(&full[s], nc * cb);
+          for (int c = 0; c < nc; ++c)
+            bulk_g2s(ring + ((size_t)s * CBS + c) * TRC, Q + (size_t)(b * CBS + c) * ld + row0, cb,
+                     &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  int it = 0;
+  for (int rb = 0; rb < nrb; ++rb) {
+    const int row0 = r0 + rb * TRC;
+    const int rows = min(TRC, r1 - row0);
+    const int lr = 64 * warp + lane;  // this lane's rows lr, lr + 32 of the stage
+    const bool ok0 = lr < rows, ok1 = lr + 32 < rows;
+    const int ws = rb & 1;
+    mbar_wait(&wzfull[ws], (rb >> 1) & 1);
+    const double* wzb = wz + (size_t)ws * 2 * TRC;
+    const double w0 = ok0 ? wzb[lr] : 0.0, w1 = ok1 ? wzb[lr + 32] : 0.0;
+    const double z0 = ok0 ? wzb[TRC + lr] : 0.0, z1 = ok1 ? wzb[TRC + lr + 32] : 0.0;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&wzempty[ws]);
+    for (int b = 0; b < ncb; ++b, ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full[s], (it / STAGES) & 1);
+      const double* st = ring + (size_t)s * CBS * TRC;
+      const int nc = min(CBS, P - b * CBS);
+      double v[2 * CBS];
+#pragma unroll
+      for (int cc = 0; cc < CBS; ++cc) {
+        const double* qc = st + (size_t)min(cc, nc - 1) * TRC;
+        const double q0 = ok0 ? qc[lr] : 0.0, q1 = ok1 ? qc[lr + 32] : 0.0;
+        v[cc] = fma(q1, w1, q0 * w0);
+        v[CBS + cc] = fma(q1, z1, q0 * z0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      const double tot = bfly<2 * CBS>(v, lane);
+      constexpr int L2 = CBS == 8 ? 4 : CBS == 4 ? 3 : 5;
+      constexpr int SH = 5 - L2;
+      const int idx = (lane >> SH) & (2 * CBS - 1), col = b * CBS + (idx % CBS);
+      if (!(lane & ((1 << SH) - 1)) && (idx % CBS) < nc) sacc[warp][(idx / CBS) * 64 + col] += tot;
+    }
+  }
+  // consumers only (the producer warp has left): named barrier over 256 threads
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  if (threadIdx.x < 2 * P) {
+    const int m = threadIdx.x / P, c = threadIdx.x % P;
+    double s = 0.0;
+    for (int q = 0; q < NW; ++q) s += sacc[q][m * 64 + c];
+    out[(size_t)blockIdx.x * 128 + threadIdx.x] = s;
+  }
+}
+
 int main() {
   const int n = 1 << 21;
   int sms = 0;
@@ -194,8 +326,12 @@ int main() {
   cudaEventCreate(&e1);
   double* o1 = new double[nblk * 128];
   double* o2 = new double[nblk * 128];
+  double* o3 = new double[nblk * 128];
+  const int smem3 = (2 * 8 * 512 + 4 * 512) * 8, smem4 = (6 * 8 * 512 + 4 * 512) * 8;
+  cudaFuncSetAttribute(v3<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+  cudaFuncSetAttribute(v3<6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4);
   for (int P : {20, 32, 40, 60}) {
-    for (int v = 0; v < 3; ++v) {
+    for (int v = 0; v < 5; ++v) {
       float best = 1e9f;
       for (int rep = 0; rep < 8; ++rep) {
         cudaMemset(flush, rep, 512 << 20);
@@ -203,6 +339,8 @@ int main() {
         if (v == 0) v0<<<nblk, NT>>>(Q, n, P, w, z, rpb, n, out);
         if (v == 1) v1<<<nblk, NT>>>(Q, n, P, w, z, rpb, n, out);
         if (v == 2) v2<<<nblk, NT>>>(Q, n, P, w, z, rpb, n, out);
+        if (v == 3) v3<2, 8><<<nblk, NT + 32, smem3>>>(Q, n, P, w, z, rpb, n, out);
+        if (v == 4) v3<6, 8><<<sms, NT + 32, smem4>>>(Q, n, P, w, z, 2 * rpb, n, out);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -211,6 +349,7 @@ int main() {
       }
       if (v == 1) cudaMemcpy(o1, out, (size_t)nblk * 128 * 8, cudaMemcpyDeviceToHost);
       if (v == 2) cudaMemcpy(o2, out, (size_t)nblk * 128 * 8, cudaMemcpyDeviceToHost);
+      if (v == 3) cudaMemcpy(o3, out, (size_t)nblk * 128 * 8, cudaMemcpyDeviceToHost);
       double gb = (double)(P + 2) * n * 8 / (best * 1e-3) / 1e9;
       printf("P=%d v%d: %.3f ms  %.0f GB/s  %s\n", P, v, best, gb, cudaGetErrorString(cudaGetLastError()));
     }
@@ -221,6 +360,13 @@ int main() {
         md = fmax(md, fabs(d) / (1e-30 + fabs(o1[b * 128 + i])));
       }
     printf("P=%d max rel diff v1 vs v2 %.2e\n", P, md);
+    md = 0.0;
+    for (int b = 0; b < nblk; ++b)
+      for (int i = 0; i < 2 * P; ++i) {
+        double d = o1[b * 128 + i] - o3[b * 128 + i];
+        md = fmax(md, fabs(d) / (1e-30 + fabs(o1[b * 128 + i])));
+      }
+    printf("P=%d max rel diff v1 vs v3 (TMA ring) %.2e\n", P, md);
   }
   return 0;
 }

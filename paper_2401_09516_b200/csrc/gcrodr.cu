@@ -760,6 +760,10 @@ __device__ __forceinline__ void spmv_rows(const int* rp, const int* ci, const do
 // |C^T r| / beta above which the cycle forms V_0 from r - C C^T r (cycle start)
 constexpr double V0_PROJ_RTOL = 1e-12;
 
+#ifndef SKR_SW1_PREFETCH
+#define SKR_SW1_PREFETCH 0  // measured: the 16 extra live registers spill into sweep 2 (C3 -27%)
+#endif
+constexpr bool SW1_PREFETCH = SKR_SW1_PREFETCH != 0;  // sweep 1: first basis batch ahead of the SpMV
 constexpr int GT_LD = 33;  // padded rows per staged Gram column (odd: conflict-free)
 constexpr int FUSE_COMB_ROWS = 4096;  // rows per CTA from which k_cycle applies the update
 constexpr int GM_MMAX = 40;  // Arnoldi length up to which the cycle end uses the DMMA Gram
@@ -901,18 +905,28 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       i = min(i, nin - 1);
       return i < kcp ? (uc ? kcp + i : i) : 2 * kcp + (i - kcp);
     };
+    // staged column c lives at basis column c (U) or c + 2 (kcap - kcp) (the
+    // right-aligned C block and V follow each other); column ncs is r
     auto src_col = [&](int c) -> const double* {
-      return c < kcp ? colU(p, c) : c < 2 * kcp ? colC(p, kcap - kcp + (c - kcp))
-                   : c < ncs ? colV(p, c - 2 * kcp) : p.r;
+      return c >= ncs ? p.r : p.basis + (size_t)(c < kcp ? c : c + 2 * (kcap - kcp)) * p.ld;
     };
-    constexpr int GPF = 8;  // the next two tiles' first elements, in flight
-    double pf[GPF], pf2[GPF];
-    const int nel = 32 * (ncs + 1);
-    auto load_tile = [&](double (&dst)[GPF], int t0) {
+    // a thread stages row pairs (16-byte loads and shared stores) of the columns
+    // (tid >> 4) + 16 k: pointers fixed for the whole pass, the next two
+    // tiles' elements in flight in registers
+    constexpr int GPF = 4;
+    double2 pf[GPF], pf2[GPF];
+    const int prr = 2 * (tid & 15), pc0 = tid >> 4;
+    auto load_tile = [&](double2 (&dst)[GPF], int t0) {
+      const int row = t0 + prr;
 #pragma unroll
       for (int k = 0; k < GPF; ++k) {
-        const int e = tid + k * NT, row = t0 + (e & 31);
-        if (e < nel) dst[k] = row < r1 ? src_col(e >> 5)[row] : 0.0;
+        const int c = pc0 + 16 * k;
+        if (c > ncs) continue;
+        const double* q = src_col(c) + row;
+        if (row + 1 < r1)
+          dst[k] = *reinterpret_cast<const double2*>(q);
+        else
+          dst[k] = make_double2(row < r1 ? q[0] : 0.0, 0.0);
       }
     };
     double psq[4] = {0.0, 0.0, 0.0, 0.0};  // |U_q|^2 (uc 0) or C_q . r (uc 1), this lane's rows
@@ -921,11 +935,10 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     for (int t0 = r0; t0 < r1; t0 += 32) {
       __syncthreads();  // the previous tile (and the coefficients) are in place / consumed
 #pragma unroll
-      for (int k = 0; k < GPF; ++k) {
-        const int e = tid + k * NT;
-        if (e < nel) stg[(e >> 5) * GM_LD + (e & 31)] = pf[k];
-      }
-      for (int e = tid + GPF * NT; e < nel; e += NT) {
+      for (int k = 0; k < GPF; ++k)
+        if (pc0 + 16 * k <= ncs)
+          *reinterpret_cast<double2*>(stg + (pc0 + 16 * k) * GM_LD + prr) = pf[k];
+      for (int e = tid + 32 * 16 * GPF; e < 32 * (ncs + 1); e += NT) {  // columns past 64 (m > 40)
         const int row = t0 + (e & 31);
         stg[(e >> 5) * GM_LD + (e & 31)] = row < r1 ? src_col(e >> 5)[row] : 0.0;
       }
@@ -953,8 +966,10 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         const int q = 8 * mb + ln;
         if (mb < nmb && q < nout) {
           double* dst = uc ? colC(p, kcap - nout + q) : colU(p, q);
-          if (row < r1) dst[row] = acc[mb][0];
-          if (row + 1 < r1) dst[row + 1] = acc[mb][1];
+          if (row + 1 < r1)
+            *reinterpret_cast<double2*>(dst + row) = make_double2(acc[mb][0], acc[mb][1]);
+          else if (row < r1)
+            dst[row] = acc[mb][0];
           if (partials) {
             if (uc)
               psq[mb] += acc[mb][0] * stg[ncs * GM_LD + rl] + acc[mb][1] * stg[ncs * GM_LD + rl + 1];
@@ -1187,6 +1202,21 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       double dgv[R];  // Jacobi pivots, loaded ahead of the SpMV's dependent chain
 #pragma unroll
       for (int i = 0; i < R; ++i) dgv[i] = p.dg ? __ldg(p.dg + row[i]) : 1.0;
+      // all CB x R loads of a batch first (no branch: columns past pb re-read
+      // column pb - 1 and their sums are dropped), then the FMAs. The first
+      // batch is issued here, ahead of the SpMV: its round trip then overlaps
+      // the SpMV's instead of following it (the compiler cannot hoist the loads
+      // over the store of z)
+      double qv[CB][R];
+      auto load_batch = [&](int c0) {
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+          const double* Qc = Qb + (size_t)min(c0 + cc, pb - 1) * ld + base;
+#pragma unroll
+          for (int i = 0; i < R; ++i) qv[cc][i] = ok[i] ? Qc[32 * i] : 0.0;
+        }
+      };
+      if (SW1_PREFETCH && pb > 0) load_batch(0);
       if (do_spmv && GPC) {
 #pragma unroll
         for (int i = 0; i < R; ++i) z[i] = p.z[row[i]];  // M^-1 A V_t of the phase above
@@ -1219,15 +1249,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
         ze += z[i] * z[i];
       }
       for (int c0 = 0; c0 < pb; c0 += CB) {
-        // all CB x R loads first (no branch: columns past pb re-read column
-        // pb - 1 and their sums are dropped), then the FMAs
-        double qv[CB][R];
-#pragma unroll
-        for (int cc = 0; cc < CB; ++cc) {
-          const double* Qc = Qb + (size_t)min(c0 + cc, pb - 1) * ld + base;
-#pragma unroll
-          for (int i = 0; i < R; ++i) qv[cc][i] = ok[i] ? Qc[32 * i] : 0.0;
-        }
+        if (!SW1_PREFETCH || c0 > 0) load_batch(c0);
         double v[2 * CB];
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc) {

@@ -175,6 +175,7 @@ struct Ptrs {
   int fuse_comb;  // 1: k_cycle applies the recycle update at its start (large row slices);
                   // 0: a separate k_combine launch after every dense update
   int gram_half;  // 1: the DMMA cross-Gram computes What^T U only (What^T V = [0; I])
+  int upd_direct;  // k_update: B fragments straight from global memory (no shared tile)
   PcHeader* pch;  // general preconditioner (SOR / ILU0 / IC0 / block Jacobi) or nullptr; with
                   // it dg is nullptr and op(v) = M^-1 (A v) runs as an SpMV phase followed by
                   // the level-scheduled sweeps of precond.cuh
@@ -815,6 +816,294 @@ inline CycleSmemLayout cycle_smem_layout(int m, int kcap) {
 #endif
 constexpr size_t CYCLE_DSMEM_BUDGET = SKR_CYCLE_DSMEM_KB * 1024;
 
+// The recycle update of a finished cycle (gcrodr.py:444-467), in place, over this
+// CTA's rows [blockIdx.x * rpb, ...): U <- [U | V_0..V_{j-1}] coefU, C <- [C | V_0..V_j]
+// coefC (coefficients of the dense kernel's P_CYCLE), on the fp64 tensor cores:
+// DMMA m8n8k4 with A = coef^T (outputs x inputs) and B = the staged 32-row tile
+// (inputs x rows), so no output padding beyond 8 columns is wasted. With
+// `partials`, the next cycle start's per-CTA sums C^T r and |U_c|^2 are formed from
+// the new columns in the same pass. Called from k_cycle (fused) or k_update.
+__device__ __forceinline__ void recycle_update_dmma(const Ptrs& p, double* cdyn, double* bred,
+                                                    bool partials) {
+  State* st = p.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, blk = blockIdx.x;
+  const int kcap = p.kcap, m = st->m;
+  const int r0 = blk * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  const int kcp = st->kc_prev, jj = st->j;
+  const int nout = st->upd ? st->k_new : 0;
+  double* part0 = p.part + (size_t)COMB_PART0 * GRID_MAX + blk;
+  if (nout == 0) {  // no update: the next cycle's partials from U, C as they are
+    if (!partials) return;
+    for (int c = 0; c < kcp; ++c) {
+      const double* Cc = colC(p, kcap - kcp + c);
+      const double* Uc = colU(p, c);
+      double s1 = 0.0, s2 = 0.0;
+      for (int row = r0 + tid; row < r1; row += NT) {
+        s1 += Cc[row] * p.r[row];
+        const double u = Uc[row];
+        s2 += u * u;
+      }
+      const double t1 = block_sum(s1, bred);
+      const double t2 = block_sum(s2, bred);
+      if (tid == 0) {
+        part0[(size_t)c * GRID_MAX] = t1;
+        part0[(size_t)(kcp + c) * GRID_MAX] = t2;
+      }
+    }
+    return;
+  }
+  const int nin_u = kcp + jj, nin_c = kcp + jj + 1;
+  const int ncs = 2 * kcp + jj + 1;  // staged [U (kcp) | C (kcp) | V_0..V_jj], then r
+  const int cld = comb_ld(m);
+  const int kbn = ((nout + 7) >> 3) * 8, nmb = kbn >> 3;  // padded outputs, <= 4 blocks
+  double* stg = cdyn;
+  double* cfs = cdyn + p.sm_cmb;
+  for (int e = tid; e < 2 * kbn * cld; e += NT) {  // cfs[(h kbn + q) cld + i] = coef_h[i][q]
+    const int i = e % cld, q = (e / cld) % kbn, h = e / (cld * kbn);
+    cfs[e] = (q < nout && i < (h ? nin_c : nin_u)) ? (h ? st->coefC : st->coefU)[i + q * LDC]
+                                                   : 0.0;
+  }
+  // warp: outputs of U (uc 0) or C (uc 1), rows 8 nbr .. 8 nbr + 7 of a tile
+  const int uc = warp >> 2, nbr = warp & 3, ln = lane >> 2, lk = lane & 3;
+  const int nin = uc ? nin_c : nin_u, nks = (nin + 3) >> 2;
+  const double* cf = cfs + (size_t)(uc * kbn + ln) * cld + lk;  // A: coef^T[8 mb + ln][4 ks + lk]
+  auto scol = [&](int i) -> int {  // staged column of input i (padding clamped)
+    i = min(i, nin - 1);
+    return i < kcp ? (uc ? kcp + i : i) : 2 * kcp + (i - kcp);
+  };
+  // staged column c lives at basis column c (U) or c + 2 (kcap - kcp) (the
+  // right-aligned C block and V follow each other); column ncs is r
+  auto src_col = [&](int c) -> const double* {
+    return c >= ncs ? p.r : p.basis + (size_t)(c < kcp ? c : c + 2 * (kcap - kcp)) * p.ld;
+  };
+  // a thread stages row pairs (16-byte loads and shared stores) of the columns
+  // (tid >> 4) + 16 k: pointers fixed for the whole pass, the next two
+  // tiles' elements in flight in registers
+  constexpr int GPF = 4;
+  double2 pf[GPF], pf2[GPF];
+  const int prr = 2 * (tid & 15), pc0 = tid >> 4;
+  auto load_tile = [&](double2 (&dst)[GPF], int t0) {
+    const int row = t0 + prr;
+#pragma unroll
+    for (int k = 0; k < GPF; ++k) {
+      const int c = pc0 + 16 * k;
+      if (c > ncs) continue;
+      const double* q = src_col(c) + row;
+      if (row + 1 < r1)
+        dst[k] = *reinterpret_cast<const double2*>(q);
+      else
+        dst[k] = make_double2(row < r1 ? q[0] : 0.0, 0.0);
+    }
+  };
+  double psq[4] = {0.0, 0.0, 0.0, 0.0};  // |U_q|^2 (uc 0) or C_q . r (uc 1), this lane's rows
+  if (r0 < r1) load_tile(pf, r0);
+  if (r0 + 32 < r1) load_tile(pf2, r0 + 32);
+  for (int t0 = r0; t0 < r1; t0 += 32) {
+    __syncthreads();  // the previous tile (and the coefficients) are in place / consumed
+#pragma unroll
+    for (int k = 0; k < GPF; ++k)
+      if (pc0 + 16 * k <= ncs)
+        *reinterpret_cast<double2*>(stg + (pc0 + 16 * k) * GM_LD + prr) = pf[k];
+    for (int e = tid + 32 * 16 * GPF; e < 32 * (ncs + 1); e += NT) {  // columns past 64 (m > 40)
+      const int row = t0 + (e & 31);
+      stg[(e >> 5) * GM_LD + (e & 31)] = row < r1 ? src_col(e >> 5)[row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < GPF; ++k) pf[k] = pf2[k];
+    if (t0 + 64 < r1) load_tile(pf2, t0 + 64);
+    double acc[4][2];
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
+    for (int ks = 0; ks < nks; ++ks) {
+      const double bf = stg[scol(4 * ks + lk) * GM_LD + 8 * nbr + ln];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb)
+        if (mb < nmb)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[mb][0]), "+d"(acc[mb][1])
+              : "d"(cf[(size_t)mb * 8 * cld + 4 * ks]), "d"(bf));
+    }
+    // D[output 8 mb + ln][row 8 nbr + 2 lk + e]
+    const int rl = 8 * nbr + 2 * lk, row = t0 + rl;
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) {
+      const int q = 8 * mb + ln;
+      if (mb < nmb && q < nout) {
+        double* dst = uc ? colC(p, kcap - nout + q) : colU(p, q);
+        if (row + 1 < r1)
+          *reinterpret_cast<double2*>(dst + row) = make_double2(acc[mb][0], acc[mb][1]);
+        else if (row < r1)
+          dst[row] = acc[mb][0];
+        if (partials) {
+          if (uc)
+            psq[mb] += acc[mb][0] * stg[ncs * GM_LD + rl] + acc[mb][1] * stg[ncs * GM_LD + rl + 1];
+          else
+            psq[mb] += acc[mb][0] * acc[mb][0] + acc[mb][1] * acc[mb][1];
+        }
+      }
+    }
+  }
+  if (partials) {  // lanes of an output, then the 4 row-block warps, in a fixed order
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) {
+      psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 1);
+      psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 2);
+    }
+    __syncthreads();
+    double* red = stg;
+    if (lk == 0)
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) red[(uc * 4 + nbr) * 32 + 8 * mb + ln] = psq[mb];
+    __syncthreads();
+    for (int e = tid; e < 2 * nout; e += NT) {
+      const int h = e / nout, q = e % nout;  // h 1: C^T r, h 0: |U|^2
+      const double* rq = red + h * 4 * 32 + q;
+      part0[(size_t)(h ? q : nout + q) * GRID_MAX] = ((rq[0] + rq[32]) + rq[64]) + rq[96];
+    }
+  }
+  __syncthreads();
+}
+
+// The update without the shared-memory tile (k_update): every warp loads its
+// own B fragments straight from the basis (lane (ln, lk): input column
+// 4 ks + lk, row 8 nbr + ln of the tile: four 64-byte pieces per load, every
+// sector used), one tile ahead in registers, so the warps never meet at a
+// block barrier and one warp's DMMAs overlap the others' loads. Rows are owned
+// by a warp (block nbr of 8 rows, U or C outputs), the in-place update needs
+// no ordering between warps. NKS: k-steps (4 inputs each) compiled in.
+template <int NKS>
+__device__ __forceinline__ void recycle_update_direct(const Ptrs& p, double* cdyn, double* bred,
+                                                      bool partials) {
+  State* st = p.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, blk = blockIdx.x;
+  const int kcap = p.kcap, m = st->m;
+  const int r0 = blk * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  const int kcp = st->kc_prev, jj = st->j;
+  const int nout = st->upd ? st->k_new : 0;
+  double* part0 = p.part + (size_t)COMB_PART0 * GRID_MAX + blk;
+  const int nin_u = kcp + jj, nin_c = kcp + jj + 1;
+  const int cld = comb_ld(m);
+  const int kbn = ((nout + 7) >> 3) * 8, nmb = kbn >> 3;  // padded outputs, <= 4 blocks
+  double* cfs = cdyn;
+  for (int e = tid; e < 2 * kbn * cld; e += NT) {  // cfs[(h kbn + q) cld + i] = coef_h[i][q]
+    const int i = e % cld, q = (e / cld) % kbn, h = e / (cld * kbn);
+    cfs[e] = (q < nout && i < (h ? nin_c : nin_u)) ? (h ? st->coefC : st->coefU)[i + q * LDC]
+                                                   : 0.0;
+  }
+  __syncthreads();
+  const int uc = warp >> 2, nbr = warp & 3, ln = lane >> 2, lk = lane & 3;
+  const int nin = uc ? nin_c : nin_u, nks = (nin + 3) >> 2;
+  const double* cf = cfs + (size_t)(uc * kbn + ln) * cld + lk;  // A: coef^T[8 mb + ln][4 ks + lk]
+  // input i of this warp's product: U column i (uc 0, i < kcp), else the
+  // contiguous [C | V] range (basis column i + 2 kcap - kcp)
+  const size_t ld = p.ld;
+  auto in_col = [&](int i) -> const double* {
+    i = min(i, nin - 1);
+    return p.basis + (size_t)((uc == 0 && i < kcp) ? i : i + 2 * kcap - kcp) * ld;
+  };
+  const int rb = 8 * nbr + ln;  // B fragment row of the tile
+  double bcur[NKS], bnext[NKS];
+  auto load_b = [&](double (&dst)[NKS], int t0) {
+    const int row = t0 + rb;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks)
+      if (ks < nks) dst[ks] = row < r1 ? in_col(4 * ks + lk)[row] : 0.0;
+  };
+  double psq[4] = {0.0, 0.0, 0.0, 0.0};  // |U_q|^2 (uc 0) or C_q . r (uc 1), this lane's rows
+  if (r0 < r1) load_b(bnext, r0);
+  for (int t0 = r0; t0 < r1; t0 += 32) {
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) bcur[ks] = bnext[ks];
+    if (t0 + 32 < r1) load_b(bnext, t0 + 32);
+    const int rl = 8 * nbr + 2 * lk, row = t0 + rl;  // D fragment rows
+    double2 rv = make_double2(0.0, 0.0);
+    if (partials && uc) {
+      if (row + 1 < r1)
+        rv = *reinterpret_cast<const double2*>(p.r + row);
+      else if (row < r1)
+        rv.x = p.r[row];
+    }
+    double acc[4][2];
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks)
+      if (ks < nks) {
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+          if (mb < nmb)
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[mb][0]), "+d"(acc[mb][1])
+                : "d"(cf[(size_t)mb * 8 * cld + 4 * ks]), "d"(bcur[ks]));
+      }
+    // D[output 8 mb + ln][row 8 nbr + 2 lk + e]
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) {
+      const int q = 8 * mb + ln;
+      if (mb < nmb && q < nout) {
+        double* dst = uc ? colC(p, kcap - nout + q) : colU(p, q);
+        if (row + 1 < r1)
+          *reinterpret_cast<double2*>(dst + row) = make_double2(acc[mb][0], acc[mb][1]);
+        else if (row < r1)
+          dst[row] = acc[mb][0];
+        if (partials) {
+          if (uc)
+            psq[mb] += acc[mb][0] * rv.x + acc[mb][1] * rv.y;
+          else
+            psq[mb] += acc[mb][0] * acc[mb][0] + acc[mb][1] * acc[mb][1];
+        }
+      }
+    }
+  }
+  if (partials) {  // lanes of an output, then the 4 row-block warps, in a fixed order
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) {
+      psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 1);
+      psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 2);
+    }
+    __syncthreads();  // the coefficients are consumed
+    double* red = cdyn;
+    if (lk == 0)
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) red[(uc * 4 + nbr) * 32 + 8 * mb + ln] = psq[mb];
+    __syncthreads();
+    for (int e = tid; e < 2 * nout; e += NT) {
+      const int h = e / nout, q = e % nout;  // h 1: C^T r, h 0: |U|^2
+      const double* rq = red + h * 4 * 32 + q;
+      part0[(size_t)(h ? q : nout + q) * GRID_MAX] = ((rq[0] + rq[32]) + rq[64]) + rq[96];
+    }
+  }
+  (void)bred;
+}
+
+// The same update as its own launch (host: SKR_FUSE_COMB=2), nblk CTAs (the
+// chain's share of the SMs) on the slices of the cycle kernel, with its own
+// register allocation; partials in the k_combine protocol (comb_part = 1).
+__global__ void __launch_bounds__(NT, 2) k_update(Ptrs p) {
+  State* st = p.st;
+  if (!st->ran) return;  // nothing ran since the last update (look-ahead launch)
+  extern __shared__ double cdyn[];
+  __shared__ double bred[3 * NW];
+  const bool partials = !st->done;
+  const int nout = st->upd ? st->k_new : 0;
+  const int nks = (st->kc_prev + st->j + 1 + 3) >> 2;
+  if (nout == 0 || p.upd_direct == 0)
+    recycle_update_dmma(p, cdyn, bred, partials);  // (also: no update, partials only)
+  else if (nks <= 8)
+    recycle_update_direct<8>(p, cdyn, bred, partials);
+  else if (nks <= 12)
+    recycle_update_direct<12>(p, cdyn, bred, partials);
+  else
+    recycle_update_direct<16>(p, cdyn, bred, partials);
+  if (partials && blockIdx.x == 0 && threadIdx.x == 0) {
+    st->comb_part = 1;
+    st->comb_nblk = gridDim.x;
+  }
+}
+
 // R = rows per lane in the Arnoldi sweeps: warp-owned tiles of 32 R consecutive
 // rows; every lane keeps its rows' w = V_t and z = op(V_t) in registers.
 #ifndef SKR_CYCLE_MINB
@@ -855,150 +1144,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     }
   };
 
-  // ---- the previous cycle's recycle update (gcrodr.py:444-467), in place ------
-  // U <- [U | V_0..V_{j-1}] coefU, C <- [C | V_0..V_j] coefC (coefficients of
-  // the dense kernel's P_CYCLE), over this CTA's rows, on the fp64 tensor
-  // cores: DMMA m8n8k4 with A = coef^T (outputs x inputs) and B = the staged
-  // 32-row tile (inputs x rows), so no output padding beyond 8 columns is
-  // wasted. With `partials`, the next cycle start's per-CTA sums C^T r and
-  // |U_c|^2 are formed from the new columns in the same pass.
-  auto apply_update = [&](bool partials) {
-    const int kcp = st->kc_prev, jj = st->j;
-    const int nout = st->upd ? st->k_new : 0;
-    double* part0 = p.part + (size_t)COMB_PART0 * GRID_MAX + blk;
-    if (nout == 0) {  // no update: the next cycle's partials from U, C as they are
-      if (!partials) return;
-      for (int c = 0; c < kcp; ++c) {
-        const double* Cc = colC(p, kcap - kcp + c);
-        const double* Uc = colU(p, c);
-        double s1 = 0.0, s2 = 0.0;
-        for (int row = r0 + tid; row < r1; row += NT) {
-          s1 += Cc[row] * p.r[row];
-          const double u = Uc[row];
-          s2 += u * u;
-        }
-        const double t1 = block_sum(s1, S.bred);
-        const double t2 = block_sum(s2, S.bred);
-        if (tid == 0) {
-          part0[(size_t)c * GRID_MAX] = t1;
-          part0[(size_t)(kcp + c) * GRID_MAX] = t2;
-        }
-      }
-      return;
-    }
-    const int nin_u = kcp + jj, nin_c = kcp + jj + 1;
-    const int ncs = 2 * kcp + jj + 1;  // staged [U (kcp) | C (kcp) | V_0..V_jj], then r
-    const int cld = comb_ld(m);
-    const int kbn = ((nout + 7) >> 3) * 8, nmb = kbn >> 3;  // padded outputs, <= 4 blocks
-    double* stg = cdyn;
-    double* cfs = cdyn + p.sm_cmb;
-    for (int e = tid; e < 2 * kbn * cld; e += NT) {  // cfs[(h kbn + q) cld + i] = coef_h[i][q]
-      const int i = e % cld, q = (e / cld) % kbn, h = e / (cld * kbn);
-      cfs[e] = (q < nout && i < (h ? nin_c : nin_u)) ? (h ? st->coefC : st->coefU)[i + q * LDC]
-                                                     : 0.0;
-    }
-    // warp: outputs of U (uc 0) or C (uc 1), rows 8 nbr .. 8 nbr + 7 of a tile
-    const int uc = warp >> 2, nbr = warp & 3, ln = lane >> 2, lk = lane & 3;
-    const int nin = uc ? nin_c : nin_u, nks = (nin + 3) >> 2;
-    const double* cf = cfs + (size_t)(uc * kbn + ln) * cld + lk;  // A: coef^T[8 mb + ln][4 ks + lk]
-    auto scol = [&](int i) -> int {  // staged column of input i (padding clamped)
-      i = min(i, nin - 1);
-      return i < kcp ? (uc ? kcp + i : i) : 2 * kcp + (i - kcp);
-    };
-    // staged column c lives at basis column c (U) or c + 2 (kcap - kcp) (the
-    // right-aligned C block and V follow each other); column ncs is r
-    auto src_col = [&](int c) -> const double* {
-      return c >= ncs ? p.r : p.basis + (size_t)(c < kcp ? c : c + 2 * (kcap - kcp)) * p.ld;
-    };
-    // a thread stages row pairs (16-byte loads and shared stores) of the columns
-    // (tid >> 4) + 16 k: pointers fixed for the whole pass, the next two
-    // tiles' elements in flight in registers
-    constexpr int GPF = 4;
-    double2 pf[GPF], pf2[GPF];
-    const int prr = 2 * (tid & 15), pc0 = tid >> 4;
-    auto load_tile = [&](double2 (&dst)[GPF], int t0) {
-      const int row = t0 + prr;
-#pragma unroll
-      for (int k = 0; k < GPF; ++k) {
-        const int c = pc0 + 16 * k;
-        if (c > ncs) continue;
-        const double* q = src_col(c) + row;
-        if (row + 1 < r1)
-          dst[k] = *reinterpret_cast<const double2*>(q);
-        else
-          dst[k] = make_double2(row < r1 ? q[0] : 0.0, 0.0);
-      }
-    };
-    double psq[4] = {0.0, 0.0, 0.0, 0.0};  // |U_q|^2 (uc 0) or C_q . r (uc 1), this lane's rows
-    if (r0 < r1) load_tile(pf, r0);
-    if (r0 + 32 < r1) load_tile(pf2, r0 + 32);
-    for (int t0 = r0; t0 < r1; t0 += 32) {
-      __syncthreads();  // the previous tile (and the coefficients) are in place / consumed
-#pragma unroll
-      for (int k = 0; k < GPF; ++k)
-        if (pc0 + 16 * k <= ncs)
-          *reinterpret_cast<double2*>(stg + (pc0 + 16 * k) * GM_LD + prr) = pf[k];
-      for (int e = tid + 32 * 16 * GPF; e < 32 * (ncs + 1); e += NT) {  // columns past 64 (m > 40)
-        const int row = t0 + (e & 31);
-        stg[(e >> 5) * GM_LD + (e & 31)] = row < r1 ? src_col(e >> 5)[row] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < GPF; ++k) pf[k] = pf2[k];
-      if (t0 + 64 < r1) load_tile(pf2, t0 + 64);
-      double acc[4][2];
-#pragma unroll
-      for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
-      for (int ks = 0; ks < nks; ++ks) {
-        const double bf = stg[scol(4 * ks + lk) * GM_LD + 8 * nbr + ln];
-#pragma unroll
-        for (int mb = 0; mb < 4; ++mb)
-          if (mb < nmb)
-            asm volatile(
-                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                : "+d"(acc[mb][0]), "+d"(acc[mb][1])
-                : "d"(cf[(size_t)mb * 8 * cld + 4 * ks]), "d"(bf));
-      }
-      // D[output 8 mb + ln][row 8 nbr + 2 lk + e]
-      const int rl = 8 * nbr + 2 * lk, row = t0 + rl;
-#pragma unroll
-      for (int mb = 0; mb < 4; ++mb) {
-        const int q = 8 * mb + ln;
-        if (mb < nmb && q < nout) {
-          double* dst = uc ? colC(p, kcap - nout + q) : colU(p, q);
-          if (row + 1 < r1)
-            *reinterpret_cast<double2*>(dst + row) = make_double2(acc[mb][0], acc[mb][1]);
-          else if (row < r1)
-            dst[row] = acc[mb][0];
-          if (partials) {
-            if (uc)
-              psq[mb] += acc[mb][0] * stg[ncs * GM_LD + rl] + acc[mb][1] * stg[ncs * GM_LD + rl + 1];
-            else
-              psq[mb] += acc[mb][0] * acc[mb][0] + acc[mb][1] * acc[mb][1];
-          }
-        }
-      }
-    }
-    if (partials) {  // lanes of an output, then the 4 row-block warps, in a fixed order
-#pragma unroll
-      for (int mb = 0; mb < 4; ++mb) {
-        psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 1);
-        psq[mb] += __shfl_xor_sync(0xffffffffu, psq[mb], 2);
-      }
-      __syncthreads();
-      double* red = stg;
-      if (lk == 0)
-#pragma unroll
-        for (int mb = 0; mb < 4; ++mb) red[(uc * 4 + nbr) * 32 + 8 * mb + ln] = psq[mb];
-      __syncthreads();
-      for (int e = tid; e < 2 * nout; e += NT) {
-        const int h = e / nout, q = e % nout;  // h 1: C^T r, h 0: |U|^2
-        const double* rq = red + h * 4 * 32 + q;
-        part0[(size_t)(h ? q : nout + q) * GRID_MAX] = ((rq[0] + rq[32]) + rq[64]) + rq[96];
-      }
-    }
-    __syncthreads();
-  };
+  auto apply_update = [&](bool partials) { recycle_update_dmma(p, cdyn, S.bred, partials); };
   if (st->done) {
     // the look-ahead launch after the final cycle applies that cycle's update
     // (the next solve's refresh reads U), then leaves
@@ -1610,7 +1756,8 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   // the register-tiled CUDA-core Gram after the residual (below).
   const bool gmma = defl && m <= GM_MMAX;
   auto tile_col = [&](int c) -> const double* {  // staged columns [U (kc) | C (kc) | V (j)]
-    return (c < kc) ? colU(p, c) : (c < 2 * kc) ? colC(p, kcap - kc + (c - kc)) : colV(p, c - 2 * kc);
+    // basis column c (U) or c + 2 (kcap - kc): the right-aligned C block and V are adjacent
+    return p.basis + (size_t)(c < kc ? c : c + 2 * (kcap - kc)) * ld;
   };
   if (gmma) {
     constexpr int GL = GM_LD;  // == 4 (mod 16) doubles: conflict-free fragment loads
@@ -2384,6 +2531,8 @@ static int ensure_dev(DevInfo** out) {
       nb = std::min(nb, nbv);
     }
     d.cycle_blocks_per_sm = nb;
+    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)CYCLE_DSMEM_BUDGET);
     const int combine_smem = 2 * LDC * KMAX * (int)sizeof(double);
     cudaFuncSetAttribute(k_combine<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
     cudaFuncSetAttribute(k_combine<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, combine_smem);
@@ -2646,7 +2795,13 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   // are long; with short ones (C1 at 64 CTAs: 1,024 rows) a separate
   // k_combine on every SM has the lower latency (measured: C1 -5% fused)
   p.fuse_comb = p.rpb >= FUSE_COMB_ROWS ? 1 : 0;
-  if (const char* e = getenv("SKR_FUSE_COMB")) p.fuse_comb = atoi(e) ? 1 : 0;
+  p.upd_direct = 1;
+  if (const char* e = getenv("SKR_UPD_DIRECT")) p.upd_direct = atoi(e) ? 1 : 0;
+  bool kupd = false;  // the DMMA update as its own launch (k_update) instead of inside k_cycle
+  if (const char* e = getenv("SKR_FUSE_COMB")) {
+    p.fuse_comb = atoi(e) == 1 ? 1 : 0;
+    kupd = atoi(e) == 2;
+  }
   p.v0_rtol = V0_PROJ_RTOL;
   if (const char* e = getenv("SKR_V0_RTOL")) p.v0_rtol = atof(e);
   p.gram_half = 0;
@@ -2671,6 +2826,8 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     if (cycle_fixed + want <= CYCLE_DSMEM_BUDGET && !getenv("SKR_NO_CSR_CACHE")) csr_cap = want;
   }
   size_t cycle_dsmem = cycle_fixed + csr_cap;
+  const size_t upd_smem =
+      (SL.cmb + 2 * (size_t)((L.kcap + 7) / 8 * 8) * comb_ld(cfg->m)) * sizeof(double);
   int csr_cap_i = (int)csr_cap;
   const void* cycle_fn = cycle_kernel(p.pch ? 8 : cycle_rows_per_lane(p.rpb));
   int pc_target = 0, pc_stage = 0;
@@ -2786,7 +2943,10 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
       launches += 2;
       // fused: the update is applied at the start of the next k_cycle
       if (!p.fuse_comb) {
-        launch_combine(kt, p, ncomb, 1, s);
+        if (kupd)
+          k_update<<<nblk, NT, upd_smem, s>>>(p);
+        else
+          launch_combine(kt, p, ncomb, 1, s);
         ++launches;
       }
       if (diag) {

@@ -201,3 +201,69 @@ def test_gpu_sequence_with_general_preconditioner(kind):
         assert res.converged[p]
         assert abs(res.iterations[p] - ref[p].iterations) <= max(1, 0.05 * ref[p].iterations)
         assert rel(res.x[p], ref[p].x) < 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["sor", "ilu0", "bjacobi"])
+def test_gpu_general_preconditioner_side_paths(kind):
+    """x0 (the preconditioned initial residual, gcrodr.py:348-351), the
+    diagnostics records (gcrodr.py:116-123, :372-376, :461-467), the CSR path
+    without the stencil form, and the native multi-chain driver, all with a
+    general preconditioner, against the oracle."""
+    import torch
+
+    skr = _skr()
+    spec = P.CONFIGS[1].reduced(n=24)
+    cfg = skr.SolverConfig(m=16, k=5, tol=1e-9, max_iter=3000)
+    ocfg = orc.Cfg(m=16, k=5, tol=1e-9, max_iter=3000)
+    rp, ci, v, b, _ = P.assemble(spec, 1)
+    A = skr.CsrMatrix(spec.N, spec.N, rp, ci, v)
+    M = skr.build_preconditioner(A, kind)
+    op = orc.Operator(rp, ci, v, spec.N, False, prec=orc.GeneralPrec(rp, ci, v, spec.N, kind))
+    # x0
+    x0 = np.random.default_rng(3).standard_normal(spec.N)
+    rep, sp0 = skr.gcrodr_solve(A, b, x0=x0, M=M, cfg=cfg)
+    ref = orc.gcrodr(op, b, ocfg, x0=x0)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+    assert rel(rep.x, ref.x) < 1e-7
+    assert abs(rep.residual_history[0] - ref.history[0]) <= 1e-10 * ref.history[0]
+    # diagnostics on a recycled solve
+    rp1, ci1, v1, b1, _ = P.assemble(spec, 2)
+    A1 = skr.CsrMatrix(spec.N, spec.N, rp1, ci1, v1)
+    M1 = skr.build_preconditioner(A1, kind)
+    op1 = orc.Operator(rp1, ci1, v1, spec.N, False,
+                       prec=orc.GeneralPrec(rp1, ci1, v1, spec.N, kind))
+    rep1, _ = skr.gcrodr_solve(A1, b1, M=M1, cfg=cfg, recycle_in=sp0, collect_diagnostics=True)
+    ref1 = orc.gcrodr(op1, b1, ocfg, U_in=sp0.U.cpu().numpy(), collect_diagnostics=True)
+    got, want = rep1.diagnostics["cycles"], ref1.info["cycles"]
+    assert [(d["stage"], d["k"]) for d in got] == [(d["stage"], d["k"]) for d in want]
+    for d, w in zip(got, want):
+        assert d["au_c"] <= max(100 * w["au_c"], 1e-9), (d, w)
+        assert d["orth"] <= max(100 * w["orth"], 1e-9), (d, w)
+    assert abs(rep1.iterations - ref1.iterations) <= 1
+    # CSR path (no stencil form): same iterations, same x to rounding
+    os.environ["SKR_NO_STENCIL"] = "1"
+    try:
+        Mn = skr.build_preconditioner(A, kind)
+        repn, _ = skr.gcrodr_solve(A, b, x0=x0, M=Mn, cfg=cfg)
+    finally:
+        del os.environ["SKR_NO_STENCIL"]
+    assert repn.iterations == rep.iterations and rel(repn.x, rep.x) < 1e-12
+    # native chains driver: two chains of two device-resident systems
+    systems = []
+    for i in range(4):
+        dA, bd, _ = P.assemble_device(spec, i)
+        systems.append((dA.with_diag(None), bd))
+    torch.cuda.synchronize()
+    res = skr.solve_chains(systems, list(range(4)), cfg, kind, [[0, 1], [2, 3]], keep_x="device")
+    for c, chunk in enumerate(([0, 1], [2, 3])):
+        U = None
+        for p_, i in enumerate(chunk):
+            rpi, cii, vi, bi, _ = P.assemble(spec, i)
+            opi = orc.Operator(rpi, cii, vi, spec.N, False,
+                               prec=orc.GeneralPrec(rpi, cii, vi, spec.N, kind))
+            r = orc.gcrodr(opi, bi, ocfg, U_in=U)
+            U = r.U
+            assert res[c].converged[p_]
+            assert abs(res[c].iterations[p_] - r.iterations) <= 1, (c, p_)
+            assert rel(res[c].x[p_].cpu().numpy(), r.x) < 1e-6

@@ -368,5 +368,31 @@ int main() {
       }
     printf("P=%d max rel diff v1 vs v3 (TMA ring) %.2e\n", P, md);
   }
+  // leading-dimension padding: column stride 2^21 doubles (16 MiB) vs padded
+  {
+    double* Qp;
+    const int P = 40;
+    cudaMalloc(&Qp, ((size_t)n + 4096) * PM * 8);
+    for (int pad : {0, 64, 192, 448, 1088, 2112}) {
+      const int ldp = n + pad;
+      for (int c = 0; c < PM; ++c) cudaMemcpy(Qp + (size_t)c * ldp, h, n * 8, cudaMemcpyHostToDevice);
+      for (int v : {1, 3}) {
+        float best = 1e9f;
+        for (int rep = 0; rep < 8; ++rep) {
+          cudaMemset(flush, rep, 512 << 20);
+          cudaEventRecord(e0);
+          if (v == 1) v1<<<nblk, NT>>>(Qp, ldp, P, w, z, rpb, n, out);
+          if (v == 3) v3<2, 8><<<nblk, NT + 32, smem3>>>(Qp, ldp, P, w, z, rpb, n, out);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          best = ms < best ? ms : best;
+        }
+        printf("ld pad %4d doubles, P=40 v%d: %.3f ms  %.0f GB/s\n", pad, v, best,
+               (double)(P + 2) * n * 8 / (best * 1e-3) / 1e9);
+      }
+    }
+  }
   return 0;
 }

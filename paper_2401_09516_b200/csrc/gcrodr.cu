@@ -1144,7 +1144,11 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
     }
   };
 
+#ifdef SKR_NO_FUSED_UPDATE  // build without the in-kernel update (k_update only): A/B of the register allocation
+  auto apply_update = [&](bool) {};
+#else
   auto apply_update = [&](bool partials) { recycle_update_dmma(p, cdyn, S.bred, partials); };
+#endif
   if (st->done) {
     // the look-ahead launch after the final cycle applies that cycle's update
     // (the next solve's refresh reads U), then leaves
@@ -2802,6 +2806,12 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
     p.fuse_comb = atoi(e) == 1 ? 1 : 0;
     kupd = atoi(e) == 2;
   }
+#ifdef SKR_NO_FUSED_UPDATE
+  if (p.fuse_comb) {
+    p.fuse_comb = 0;
+    kupd = true;
+  }
+#endif
   p.v0_rtol = V0_PROJ_RTOL;
   if (const char* e = getenv("SKR_V0_RTOL")) p.v0_rtol = atof(e);
   p.gram_half = 0;

@@ -18,7 +18,7 @@
 namespace skr {
 
 struct PcLayout {
-  size_t fval, dpos, lptr[2], lrows[2], lev[2], cur[2], lu, perm, total;
+  size_t fval, dpos, lptr[2], lrows[2], lev[2], cur[2], prp[2], pdiv[2], pci, pval, lu, perm, total;
 };
 
 static inline size_t pc_align(size_t x) { return (x + 255) / 256 * 256; }
@@ -49,7 +49,16 @@ static PcLayout pc_layout(int kind, int n, int nnz, int bs) {
       off = pc_align(off + (size_t)n * sizeof(int));
       L.cur[h] = off;
       off = pc_align(off + ((size_t)n + 2) * sizeof(int));
+      L.prp[h] = off;
+      off = pc_align(off + ((size_t)n + 2) * sizeof(int));
+      L.pdiv[h] = off;
+      off = pc_align(off + (size_t)n * sizeof(double));
     }
+    // packed off-diagonal entries of both schedules: lower first, then upper
+    L.pci = off;
+    off = pc_align(off + ((size_t)nnz + 64) * sizeof(int));
+    L.pval = off;
+    off = pc_align(off + ((size_t)nnz + 64) * sizeof(double));
   }
   L.total = off;
   return L;
@@ -68,6 +77,10 @@ struct PcBuildArgs {
   int* lrows[2];
   int* lev[2];
   int* cur[2];
+  int* prp[2];
+  double* pdiv[2];
+  int* pci;
+  double* pval;
   int bs, nb;
   double* lu;
   int* perm;
@@ -375,6 +388,42 @@ __global__ void __launch_bounds__(NT) k_pc_build(PcBuildArgs a) {
       }
     }
   }
+  // ---- S6: the sweeps' operands in level order (precond.cuh) ----------------
+  PC_SYNC();
+  for (int hh = 0; hh < (need_up ? 2 : 1); ++hh)  // off-diagonal counts per position
+    for (int e = gtid; e < n; e += gthreads) {
+      const int i = a.lrows[hh][e], d = a.dpos[i];
+      a.cur[hh][e] = hh ? __ldg(a.rp + i + 1) - d - 1 : d - __ldg(a.rp + i);
+    }
+  PC_SYNC();
+  if (blockIdx.x == 0) cta_scan(a.cur[0], a.prp[0], n, s_tmp);
+  if (need_up && blockIdx.x == (gridDim.x > 1 ? 1 : 0)) cta_scan(a.cur[1], a.prp[1], n, s_tmp);
+  PC_SYNC();
+  const int nlo = a.prp[0][n];
+  for (int hh = 0; hh < (need_up ? 2 : 1); ++hh) {
+    // PcView divides every row: 1 for the unit sweep (ILU(0) lower)
+    const bool unit = a.kind == PC_ILU0 && hh == 0;
+    const int base = hh ? nlo : 0;
+    for (int e = gtid; e < n; e += gthreads) {
+      const int i = a.lrows[hh][e], d = a.dpos[i];
+      const int q0 = hh ? d + 1 : __ldg(a.rp + i), q1 = hh ? __ldg(a.rp + i + 1) : d;
+      int w = base + a.prp[hh][e];
+      for (int q = q0; q < q1; ++q, ++w) {
+        a.pci[w] = __ldg(a.ci + q);
+        a.pval[w] = a.fval[q];
+      }
+      a.pdiv[hh][e] = unit ? 1.0 : a.fval[d];
+    }
+  }
+  if (gtid == 0) {
+    PcView& v = h->v;
+    for (int q = 0; q < 2; ++q) {
+      v.prp[q] = a.prp[q];
+      v.pdiv[q] = a.pdiv[q];
+      v.pci[q] = a.pci + (q ? nlo : 0);
+      v.pval[q] = a.pval + (q ? nlo : 0);
+    }
+  }
   if (gtid == 0) {
     PcView& v = h->v;
     v.kind = a.kind;
@@ -500,7 +549,11 @@ int skr_precond_build(const skr_csr* A, int32_t kind, double omega, int32_t bloc
     a.lrows[h] = (int*)(base + L.lrows[h]);
     a.lev[h] = (int*)(base + L.lev[h]);
     a.cur[h] = (int*)(base + L.cur[h]);
+    a.prp[h] = (int*)(base + L.prp[h]);
+    a.pdiv[h] = (double*)(base + L.pdiv[h]);
   }
+  a.pci = (int*)(base + L.pci);
+  a.pval = (double*)(base + L.pval);
   a.bs = block;
   a.nb = kind == PC_BJACOBI ? (A->n + block - 1) / block : 0;
   a.lu = (double*)(base + L.lu);

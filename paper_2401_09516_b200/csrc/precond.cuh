@@ -36,6 +36,15 @@ struct PcView {
   const int* dpos;
   const int* lptr[2];   // level l of schedule h: rows lrows[h][lptr[h][l] .. lptr[h][l+1])
   const int* lrows[2];
+  // the sweeps' operands packed in level order (position e of schedule h is row
+  // lrows[h][e]): its off-diagonal factor entries pval / pci [prp[e], prp[e+1])
+  // and its divisor pdiv[e] (1 for the unit-diagonal sweep). A level's operands
+  // are contiguous and do not depend on the solution, so they are prefetched
+  // while the previous level is solved.
+  const int* prp[2];
+  const int* pci[2];
+  const double* pval[2];
+  const double* pdiv[2];
   double scale;         // ICC0: sign (1 otherwise)
   int bs, nb;           // block Jacobi: block size, number of blocks
   const double* lu;     // nb x (bs x bs) column-major LU factors (unit L below the diagonal)
@@ -59,24 +68,50 @@ struct PcHeader {
 
 // One triangular sweep over `ncols` columns of v (leading dimension ldv),
 // grid-cooperative: sync() is the caller's grid barrier (false = aborted).
+__device__ __forceinline__ void pc_prefetch_l1(const void* q) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+}
+
 template <class Sync>
 __device__ __forceinline__ bool pc_tri_sweep(const PcView& pc, int s, double* v, int ncols,
                                              size_t ldv, Sync&& sync) {
-  const int up = pc.upper[s], dm = pc.dmode[s];
+  const int up = pc.upper[s];
   const int* lptr = pc.lptr[up];
   const int* lrows = pc.lrows[up];
+  const int* prp = pc.prp[up];
+  const int* pci = pc.pci[up];
+  const double* pval = pc.pval[up];
+  const double* pdiv = pc.pdiv[up];
   const int nlev = pc.nlev[up];
+  const int n = pc.n;
   auto do_rows = [&](int lo, int nr, int first, int stride) {
     for (int it = first; it < nr * ncols; it += stride) {
-      const int i = __ldg(lrows + lo + it % nr);
+      const int e = lo + it % nr;
+      const int i = __ldg(lrows + e);
       double* col = v + (size_t)(it / nr) * ldv;
-      const int d = __ldg(pc.dpos + i);
-      const int q0 = up ? d + 1 : __ldg(pc.rp + i), q1 = up ? __ldg(pc.rp + i + 1) : d;
+      const int q0 = __ldg(prp + e), q1 = __ldg(prp + e + 1);
+      const double dv = __ldg(pdiv + e);
       double acc = col[i];
       for (int q = q0; q < q1; ++q)
-        acc = __dsub_rn(acc, __dmul_rn(__ldg(pc.fval + q), col[__ldg(pc.ci + q)]));
-      if (dm == PCD_FACTOR) acc = __ddiv_rn(acc, __ldg(pc.fval + d));
-      col[i] = acc;
+        acc = __dsub_rn(acc, __dmul_rn(__ldg(pval + q), col[__ldg(pci + q)]));
+      col[i] = __ddiv_rn(acc, dv);
+    }
+  };
+  // L1 prefetch of the operands of positions [e0, e1) (clamped to the schedule)
+  auto prefetch = [&](int e0, int e1, int q0) {
+    e1 = min(e1, n);
+    const int t = threadIdx.x;
+    if (e0 + 16 * t < e1) {
+      pc_prefetch_l1(pdiv + e0 + 16 * t);
+      pc_prefetch_l1(lrows + e0 + 16 * t);  // (16 ints: half a line; the other half by t + 1)
+      pc_prefetch_l1(prp + e0 + 16 * t);
+    }
+    // entries: about as many as positions x 4 ahead of q0, clamped to the packed total
+    const int qend = __ldg(prp + n);
+    const int q1 = min(qend, q0 + 4 * (e1 - e0) + 32);
+    if (q0 + 16 * t < q1) {
+      pc_prefetch_l1(pval + q0 + 16 * t);
+      pc_prefetch_l1(pci + q0 + 16 * t);
     }
   };
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -86,10 +121,12 @@ __device__ __forceinline__ bool pc_tri_sweep(const PcView& pc, int s, double* v,
   while (l < nlev) {
     int hi = __ldg(lptr + l + 1);
     if ((hi - lo) * ncols <= PC_NARROW) {
-      // a run of narrow levels: CTA 0 alone, a block barrier per level
+      // a run of narrow levels: CTA 0 alone, a block barrier per level; the
+      // next level's operands are on their way to L1 while this one is solved
       int l1 = l;
       while (true) {
         if (blockIdx.x == 0) {
+          prefetch(hi, hi + (hi - lo) + 32, __ldg(prp + hi));
           do_rows(lo, hi - lo, threadIdx.x, blockDim.x);
           __syncthreads();
         }

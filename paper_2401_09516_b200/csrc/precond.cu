@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "precond.cuh"
@@ -499,6 +501,7 @@ static int pc_grid(int* out) {
     // one CTA per SM: every barrier costs with the CTA count, and the sweeps
     // are latency-bound, not throughput-bound
     g_grid[dev] = std::max(1, sms * std::min(1, std::min(nb, nb2)));
+    if (const char* e = getenv("SKR_PC_GRID")) g_grid[dev] = std::max(1, std::min(g_grid[dev], atoi(e)));
   }
   *out = g_grid[dev];
   return SKR_OK;

@@ -20,7 +20,7 @@
 namespace skr {
 
 struct PcLayout {
-  size_t fval, dpos, lptr[2], lrows[2], lev[2], cur[2], prp[2], pdiv[2], pci, pval, lu, perm, total;
+  size_t fval, dpos, lptr[2], lrows[2], lev[2], cur[2], prp[2], pdiv[2], eci[2], eval[2], pci, pval, lu, perm, total;
 };
 
 static inline size_t pc_align(size_t x) { return (x + 255) / 256 * 256; }
@@ -55,6 +55,10 @@ static PcLayout pc_layout(int kind, int n, int nnz, int bs) {
       off = pc_align(off + ((size_t)n + 2) * sizeof(int));
       L.pdiv[h] = off;
       off = pc_align(off + (size_t)n * sizeof(double));
+      L.eci[h] = off;
+      off = pc_align(off + (size_t)PC_ELL * n * sizeof(int));
+      L.eval[h] = off;
+      off = pc_align(off + (size_t)PC_ELL * n * sizeof(double));
     }
     // packed off-diagonal entries of both schedules: lower first, then upper
     L.pci = off;
@@ -81,6 +85,8 @@ struct PcBuildArgs {
   int* cur[2];
   int* prp[2];
   double* pdiv[2];
+  int* eci[2];
+  double* eval[2];
   int* pci;
   double* pval;
   int bs, nb;
@@ -414,6 +420,11 @@ __global__ void __launch_bounds__(NT) k_pc_build(PcBuildArgs a) {
         a.pci[w] = __ldg(a.ci + q);
         a.pval[w] = a.fval[q];
       }
+      for (int k = 0; k < PC_ELL; ++k) {
+        const bool in = q0 + k < q1;
+        a.eci[hh][(size_t)k * n + e] = in ? __ldg(a.ci + q0 + k) : i;
+        a.eval[hh][(size_t)k * n + e] = in ? a.fval[q0 + k] : 0.0;
+      }
       a.pdiv[hh][e] = unit ? 1.0 : a.fval[d];
     }
   }
@@ -424,6 +435,8 @@ __global__ void __launch_bounds__(NT) k_pc_build(PcBuildArgs a) {
       v.pdiv[q] = a.pdiv[q];
       v.pci[q] = a.pci + (q ? nlo : 0);
       v.pval[q] = a.pval + (q ? nlo : 0);
+      v.eci[q] = a.eci[q];
+      v.eval[q] = a.eval[q];
     }
   }
   if (gtid == 0) {
@@ -554,6 +567,8 @@ int skr_precond_build(const skr_csr* A, int32_t kind, double omega, int32_t bloc
     a.cur[h] = (int*)(base + L.cur[h]);
     a.prp[h] = (int*)(base + L.prp[h]);
     a.pdiv[h] = (double*)(base + L.pdiv[h]);
+    a.eci[h] = (int*)(base + L.eci[h]);
+    a.eval[h] = (double*)(base + L.eval[h]);
   }
   a.pci = (int*)(base + L.pci);
   a.pval = (double*)(base + L.pval);

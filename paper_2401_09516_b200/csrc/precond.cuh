@@ -22,6 +22,7 @@ enum PcDiv { PCD_UNIT = 0, PCD_FACTOR = 1 };
 enum PcStatus { PCS_OK = 0, PCS_ZERO_PIVOT = 1, PCS_NOT_SYMMETRIC = 2, PCS_ABORTED = 3 };
 
 constexpr int PC_NARROW = 2 * NT;  // rows up to which a level is swept by one CTA
+constexpr int PC_ELL = 3;           // entries per row kept in the slot-major arrays
 
 struct PcView {
   int kind;        // PcKind
@@ -45,6 +46,12 @@ struct PcView {
   const int* pci[2];
   const double* pval[2];
   const double* pdiv[2];
+  // the first PC_ELL entries of every position again, slot-major (slot k of
+  // position e at [k n + e]; unused slots: the row itself with a zero value):
+  // addresses that depend on e only, so a whole level's operands are one
+  // round trip and can be loaded while the previous level is solved
+  const int* eci[2];
+  const double* eval[2];
   double scale;         // ICC0: sign (1 otherwise)
   int bs, nb;           // block Jacobi: block size, number of blocks
   const double* lu;     // nb x (bs x bs) column-major LU factors (unit L below the diagonal)
@@ -68,9 +75,13 @@ struct PcHeader {
 
 // One triangular sweep over `ncols` columns of v (leading dimension ldv),
 // grid-cooperative: sync() is the caller's grid barrier (false = aborted).
-__device__ __forceinline__ void pc_prefetch_l1(const void* q) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
-}
+// operands of one position of a schedule (solution-independent)
+struct PcRowOps {
+  int i, q0, cnt;
+  double dv;
+  int c[PC_ELL];
+  double a[PC_ELL];
+};
 
 template <class Sync>
 __device__ __forceinline__ bool pc_tri_sweep(const PcView& pc, int s, double* v, int ncols,
@@ -82,60 +93,80 @@ __device__ __forceinline__ bool pc_tri_sweep(const PcView& pc, int s, double* v,
   const int* pci = pc.pci[up];
   const double* pval = pc.pval[up];
   const double* pdiv = pc.pdiv[up];
+  const int* eci = pc.eci[up];
+  const double* eval = pc.eval[up];
   const int nlev = pc.nlev[up];
   const int n = pc.n;
+  auto load_ops = [&](int e) -> PcRowOps {
+    PcRowOps o;
+    o.i = __ldg(lrows + e);
+    o.q0 = __ldg(prp + e);
+    o.cnt = __ldg(prp + e + 1) - o.q0;
+    o.dv = __ldg(pdiv + e);
+#pragma unroll
+    for (int k = 0; k < PC_ELL; ++k) {
+      o.c[k] = __ldg(eci + (size_t)k * n + e);
+      o.a[k] = __ldg(eval + (size_t)k * n + e);
+    }
+    return o;
+  };
+  auto solve_row = [&](const PcRowOps& o, double* col) {
+    double x[PC_ELL];
+#pragma unroll
+    for (int k = 0; k < PC_ELL; ++k) x[k] = col[o.c[k]];  // (unused slots read the row itself)
+    double acc = col[o.i];
+#pragma unroll
+    for (int k = 0; k < PC_ELL; ++k)
+      if (k < o.cnt) acc = __dsub_rn(acc, __dmul_rn(o.a[k], x[k]));
+    for (int q = o.q0 + PC_ELL; q < o.q0 + o.cnt; ++q)
+      acc = __dsub_rn(acc, __dmul_rn(__ldg(pval + q), col[__ldg(pci + q)]));
+    col[o.i] = __ddiv_rn(acc, o.dv);
+  };
   auto do_rows = [&](int lo, int nr, int first, int stride) {
     for (int it = first; it < nr * ncols; it += stride) {
-      const int e = lo + it % nr;
-      const int i = __ldg(lrows + e);
-      double* col = v + (size_t)(it / nr) * ldv;
-      const int q0 = __ldg(prp + e), q1 = __ldg(prp + e + 1);
-      const double dv = __ldg(pdiv + e);
-      double acc = col[i];
-      for (int q = q0; q < q1; ++q)
-        acc = __dsub_rn(acc, __dmul_rn(__ldg(pval + q), col[__ldg(pci + q)]));
-      col[i] = __ddiv_rn(acc, dv);
-    }
-  };
-  // L1 prefetch of the operands of positions [e0, e1) (clamped to the schedule)
-  auto prefetch = [&](int e0, int e1, int q0) {
-    e1 = min(e1, n);
-    const int t = threadIdx.x;
-    if (e0 + 16 * t < e1) {
-      pc_prefetch_l1(pdiv + e0 + 16 * t);
-      pc_prefetch_l1(lrows + e0 + 16 * t);  // (16 ints: half a line; the other half by t + 1)
-      pc_prefetch_l1(prp + e0 + 16 * t);
-    }
-    // entries: about as many as positions x 4 ahead of q0, clamped to the packed total
-    const int qend = __ldg(prp + n);
-    const int q1 = min(qend, q0 + 4 * (e1 - e0) + 32);
-    if (q0 + 16 * t < q1) {
-      pc_prefetch_l1(pval + q0 + 16 * t);
-      pc_prefetch_l1(pci + q0 + 16 * t);
+      const int cidx = ncols == 1 ? 0 : it / nr;
+      solve_row(load_ops(lo + it - cidx * nr), v + (size_t)cidx * ldv);
     }
   };
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gthreads = gridDim.x * blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   int l = 0;
   int lo = __ldg(lptr);
   while (l < nlev) {
     int hi = __ldg(lptr + l + 1);
     if ((hi - lo) * ncols <= PC_NARROW) {
-      // a run of narrow levels: CTA 0 alone, a block barrier per level; the
-      // next level's operands are on their way to L1 while this one is solved
+      // a run of narrow levels: CTA 0 alone, a block barrier per level. With one
+      // column a thread's first row of the NEXT level is loaded (operands
+      // only) before this level's solution-dependent loads, so a level costs
+      // one L2 round trip instead of a chain of them.
       int l1 = l;
+      PcRowOps nxt;
+      bool have = false;
+      if (blockIdx.x == 0 && ncols == 1 && tid < hi - lo) {
+        nxt = load_ops(lo + tid);
+        have = true;
+      }
       while (true) {
+        const int nhi = l1 + 1 < nlev ? __ldg(lptr + l1 + 2) : hi;
+        const bool nnarrow = l1 + 1 < nlev && (nhi - hi) * ncols <= PC_NARROW;
         if (blockIdx.x == 0) {
-          prefetch(hi, hi + (hi - lo) + 32, __ldg(prp + hi));
-          do_rows(lo, hi - lo, threadIdx.x, blockDim.x);
+          if (ncols == 1) {
+            const PcRowOps cur = nxt;
+            const bool hcur = have;
+            have = nnarrow && tid < nhi - hi;
+            if (have) nxt = load_ops(hi + tid);
+            if (hcur) solve_row(cur, v);
+            for (int it = tid + nt; it < hi - lo; it += nt) solve_row(load_ops(lo + it), v);
+          } else {
+            do_rows(lo, hi - lo, tid, nt);
+          }
           __syncthreads();
         }
         lo = hi;
         ++l1;
-        if (l1 >= nlev) break;
-        const int h2 = __ldg(lptr + l1 + 1);
-        if ((h2 - lo) * ncols > PC_NARROW) break;
-        hi = h2;
+        if (!nnarrow) break;
+        hi = nhi;
       }
       l = l1;
     } else {

@@ -319,6 +319,91 @@ __global__ void __launch_bounds__(NT) k_gram(Ptrs p, int which, int ncols_from_s
   }
 }
 
+// The same Gram partials on the fp64 tensor cores (the refresh runs four of
+// them per system): every warp owns 32-row tiles, loads the DMMA fragments
+// straight from global memory (lane (ln, lk): column 8 b + ln, row 4 ks + lk;
+// the A fragment of column block bi is the B fragment of block bi), half a
+// tile ahead in registers, and accumulates the upper block triangle; no block
+// barrier inside the sweep. Warps are added in a fixed order at the end.
+__global__ void __launch_bounds__(NT, 2) k_gram_dmma(Ptrs p, int which, int ncols_from_state) {
+  State* st = p.st;
+  if (st->done) return;
+  const int nc = ncols_from_state == 0 ? st->ncol_a : st->ncol_b;
+  if (nc <= 0) return;
+  const double* base = which == 0 ? colU(p, 0) : colC(p, p.kcap - nc);
+  __shared__ double sg[KMAX * KMAX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ln = lane >> 2, lk = lane & 3;
+  const int r0 = blockIdx.x * p.rpb, r1 = min(p.n, r0 + p.rpb);
+  const int nb = (nc + 7) >> 3;  // <= 4 column blocks
+  constexpr int NB = KMAX / 8, HS = 4;  // k-steps (4 rows each) per half tile
+  const double* colp[NB];
+  bool cin[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    cin[b] = 8 * b + ln < nc;
+    colp[b] = base + (size_t)min(8 * b + ln, nc - 1) * p.ld + lk;
+  }
+  double acc[NB][NB][2];
+#pragma unroll
+  for (int x = 0; x < NB; ++x)
+#pragma unroll
+    for (int y = 0; y < NB; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  double cur[HS][NB], nxt[HS][NB];
+  auto load_half = [&](double (&dst)[HS][NB], int row0) {
+#pragma unroll
+    for (int ks = 0; ks < HS; ++ks) {
+      const int row = row0 + 4 * ks + lk;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (b < nb) dst[ks][b] = (cin[b] && row < r1) ? colp[b][row0 + 4 * ks] : 0.0;
+    }
+  };
+  // this warp's half tiles: rows r0 + 16 h, h = warp, warp + NW, ...
+  const int nh = (r1 - r0 + 15) >> 4;
+  if (warp < nh) load_half(nxt, r0 + 16 * warp);
+  for (int h = warp; h < nh; h += NW) {
+#pragma unroll
+    for (int ks = 0; ks < HS; ++ks)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) cur[ks][b] = nxt[ks][b];
+    if (h + NW < nh) load_half(nxt, r0 + 16 * (h + NW));
+#pragma unroll
+    for (int ks = 0; ks < HS; ++ks)
+#pragma unroll
+      for (int x = 0; x < NB; ++x)
+#pragma unroll
+        for (int y = 0; y < NB; ++y)
+          if (x <= y && y < nb)
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                : "d"(cur[ks][x]), "d"(cur[ks][y]));
+  }
+  for (int e = tid; e < KMAX * KMAX; e += NT) sg[e] = 0.0;
+  __syncthreads();
+  for (int q = 0; q < NW; ++q) {  // warps in order: a fixed summation order
+    if (warp == q)
+#pragma unroll
+      for (int x = 0; x < NB; ++x)
+#pragma unroll
+        for (int y = 0; y < NB; ++y)
+          if (x <= y && y < nb) {
+            // D[m = ln][n = 2 lk + e] of block (x, y)
+            const int i = 8 * x + ln, j = 8 * y + 2 * lk;
+            sg[i + j * KMAX] += acc[x][y][0];
+            sg[i + (j + 1) * KMAX] += acc[x][y][1];
+          }
+    __syncthreads();
+  }
+  for (int e = tid; e < nc * nc; e += NT) {
+    const int i = e % nc, j = e / nc;
+    // blocks below the diagonal were not computed: mirror (the Gram is symmetric)
+    const bool upper = (i >> 3) <= (j >> 3);
+    p.part[(size_t)e * GRID_MAX + blockIdx.x] = upper ? sg[i + j * KMAX] : sg[j + i * KMAX];
+  }
+}
+
 // C^T r partials (kc values) for the projection after the refresh
 __global__ void __launch_bounds__(NT) k_ctr(Ptrs p) {
   State* st = p.st;
@@ -2875,24 +2960,31 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const size_t dsm = dense_smem_bytes(cfg->m);
   k_dense<<<1, NT, dsm, s>>>(p, P_INIT, 0, -1);
   launches += 3;
+  static const bool gram_simple = getenv("SKR_GRAM_SIMPLE") != nullptr;
+  auto gram = [&](int which, int from_state) {
+    if (gram_simple)
+      k_gram<<<nblk, NT, 0, s>>>(p, which, from_state);
+    else
+      k_gram_dmma<<<nblk, NT, 0, s>>>(p, which, from_state);
+  };
   if (k_eff > 0) {
     // orth(U_in): CholQR pass 1 + pass 2 with QRCP(R)
-    k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
+    gram(0, 0);
     k_reduce<<<8, NT, 0, s>>>(p, 0, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 0, -1);
     launch_combine(kt, p, ncomb, 0, s);
-    k_gram<<<nblk, NT, 0, s>>>(p, 0, 0);
+    gram(0, 0);
     k_reduce<<<8, NT, 0, s>>>(p, 0, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL2, 0, -1);
     launch_combine(kt, p, ncomb, 0, s);
     // W = op(Yo) into the C block; QRCP(W) -> C, U
     k_spmm<<<nblk, NT, 0, s>>>(p);
     if (p.pch) launch_pc(1, 0);
-    k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
+    gram(1, 1);
     k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL1, 1, -1);
     launch_combine(kt, p, ncomb, 0, s);
-    k_gram<<<nblk, NT, 0, s>>>(p, 1, 1);
+    gram(1, 1);
     k_reduce<<<8, NT, 0, s>>>(p, 1, 0);
     k_dense<<<1, NT, dsm, s>>>(p, P_CHOL2, 1, -1);
     launch_combine(kt, p, ncomb, 0, s);

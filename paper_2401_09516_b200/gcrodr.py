@@ -20,7 +20,8 @@ import numpy as np
 
 from . import _lib
 from .gmres import SolveReport, SolverConfig
-from .precond import DevicePreconditioner, JacobiPreconditioner, Preconditioner
+from .precond import (DEVICE_KINDS, DevicePreconditioner, JacobiPreconditioner, Preconditioner,
+                      build_device_preconditioner)
 from .sparse import CsrMatrix, DeviceCsr
 
 __all__ = ["RecycleSpace", "GcroDrEngine", "gcrodr_solve", "harmonic_ritz_first_cycle",
@@ -215,19 +216,29 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
     cfg = cfg or SolverConfig()
     t0 = time.perf_counter()
     _lib.require_cuda()
-    jacobi = isinstance(M, JacobiPreconditioner) or getattr(M, "kind", "none") == "jacobi"
+    kind = getattr(M, "kind", "none") if M is not None else "none"
+    jacobi = isinstance(M, JacobiPreconditioner) or kind == "jacobi"
     general = M if isinstance(M, DevicePreconditioner) else None
-    if M is not None and not jacobi and general is None and getattr(M, "kind", "none") != "none":
-        raise NotImplementedError(
-            f"preconditioner {M.kind!r}: build it with this package's build_preconditioner "
-            "(the factorization lives on the device)")
+    # a preconditioner object of the reference itself (kryrec.precond.*): its
+    # kind and parameters are taken over, the factorization is redone on the
+    # device from A (the matrix the reference built it from)
+    foreign = general is None and kind in DEVICE_KINDS
+    if M is not None and not jacobi and general is None and not foreign and kind != "none":
+        raise ValueError(f"unknown preconditioner kind {kind!r}")
+
+    def jacobi_diag(host_diag):
+        if isinstance(M, JacobiPreconditioner):
+            return M.device_diag()
+        d = getattr(M, "diag", None)
+        return torch.from_numpy(np.ascontiguousarray(d if d is not None else host_diag(),
+                                                     dtype=np.float64)).to("cuda")
+
     if isinstance(A, DeviceCsr):
         dA = A
         if general is None and dA.precond is not None:
             dA = dA.with_precond(None)
         if jacobi and dA.diag is None:
-            dA = dA.with_diag(M.device_diag() if isinstance(M, JacobiPreconditioner)
-                              else None)
+            dA = dA.with_diag(jacobi_diag(lambda: _device_diag_host(dA)))
         if not jacobi and dA.diag is not None:
             dA = dA.with_diag(None)
     else:
@@ -236,9 +247,11 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
             raise ValueError("gcrodr needs a square matrix")
         dA = DeviceCsr.from_host(host, jacobi=False, stream=stream)
         if jacobi:
-            diag = (M.device_diag() if isinstance(M, JacobiPreconditioner)
-                    else torch.from_numpy(host.diagonal()).to("cuda"))
-            dA = dA.with_diag(diag)
+            dA = dA.with_diag(jacobi_diag(host.diagonal))
+    if foreign:
+        general = build_device_preconditioner(
+            dA, kind, sor_omega=float(getattr(M, "omega", 1.0)),
+            bjacobi_block=int(getattr(M, "block_size", 64)), stream=stream)
     if general is not None:
         dA = dA.with_precond(general)
     n = dA.n
@@ -322,6 +335,12 @@ def gcrodr_solve(A, b, x0=None, M: Optional[Preconditioner] = None,
         x_device=x,
     )
     return report, out_space
+
+
+def _device_diag_host(dA):
+    from .sparse import _device_diagonal
+
+    return _device_diagonal(dA.n, dA.row_ptr, dA.col_idx, dA.values).cpu().numpy()
 
 
 def _own_colmajor(X):

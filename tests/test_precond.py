@@ -324,3 +324,35 @@ def test_gpu_general_csr_preconditioners(kind, n, density):
                          orc.Cfg(m=cfg.m, k=cfg.k, tol=1e-10, max_iter=500))
         assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
         assert rel(rep.x, ref.x) < 1e-8
+
+
+@pytest.mark.gpu
+def test_gpu_accepts_reference_style_preconditioner_objects():
+    """gcrodr_solve takes over kind / omega / block_size of a preconditioner
+    object that is not this package's (the reference's classes expose the same
+    attributes, precond.py:80-145) and factors on the device."""
+    skr = _skr()
+    spec, m, k, idxs = case("darcy12")
+    rp, ci, v, b, _ = P.assemble(spec, idxs[0])
+    A = skr.CsrMatrix(spec.N, spec.N, rp, ci, v)
+    cfg = skr.SolverConfig(m=m, k=k, tol=1e-8, max_iter=5000)
+
+    class Foreign:  # stands in for kryrec.precond.SorPreconditioner etc.
+        def __init__(self, kind, **kw):
+            self.kind = kind
+            self.n = spec.N
+            self.__dict__.update(kw)
+
+    for ktag, obj in (("sor12", Foreign("sor", omega=1.2)), ("ilu0", Foreign("ilu0")),
+                      ("bjacobi", Foreign("bjacobi", block_size=20)),
+                      ("jac", Foreign("jacobi", diag=A.diagonal()))):
+        rep, _ = skr.gcrodr_solve(A, b, M=obj, cfg=cfg)
+        assert rep.converged
+        if ktag != "jac":
+            assert abs(rep.iterations - int(GOLD[f"darcy12_{ktag}_iters"][0])) <= 1
+            assert rel(rep.x, GOLD[f"darcy12_{ktag}_xs"][0]) < 1e-6
+        else:
+            ref, _ = skr.gcrodr_solve(A, b, M=skr.build_preconditioner(A, "jacobi"), cfg=cfg)
+            assert rep.iterations == ref.iterations
+    with pytest.raises(ValueError):
+        skr.gcrodr_solve(A, b, M=Foreign("ssor"), cfg=cfg)

@@ -64,6 +64,7 @@ typedef struct skr_csr {
    * When set it replaces diag: every op(v) = M^-1 (A v) and every
    * preconditioned residual solves M z = v with the stored factorization. */
   const void* precond;
+  int32_t precond_kind; /* skr_precond_kind of `precond` (0: read from the buffer) */
 } skr_csr;
 
 /* SolverConfig (gmres.py:26-43) + one launch knob. */

@@ -37,7 +37,7 @@ class SkrCsr(ctypes.Structure):
     _fields_ = [("n", c_int32), ("nnz", c_int32), ("row_ptr", c_void_p),
                 ("col_idx", c_void_p), ("values", c_void_p), ("diag", c_void_p),
                 ("stencil", c_void_p), ("sx", c_int32), ("sxy", c_int32),
-                ("precond", c_void_p)]
+                ("precond", c_void_p), ("precond_kind", c_int32)]
 
 
 class SkrSystem(ctypes.Structure):

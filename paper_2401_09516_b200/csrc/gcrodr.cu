@@ -1194,8 +1194,9 @@ __global__ void __launch_bounds__(NT, 2) k_update(Ptrs p) {
 #ifndef SKR_CYCLE_MINB
 #define SKR_CYCLE_MINB 2  // CTAs per SM the register allocation must allow
 #endif
-// GPC: a general preconditioner (p.pch) instead of none / Jacobi.
-template <int R, bool GPC>
+// GPC: a general preconditioner (p.pch) instead of none / Jacobi: 1 = the
+// triangular kinds (SOR, ILU(0), IC(0)), 2 = block Jacobi.
+template <int R, int GPC>
 __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_id, int csr_cap) {
   State* st = p.st;
   __shared__ CycleSmem S;
@@ -1413,7 +1414,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
       // z = M^-1 (A V_t): the SpMV over this CTA's rows, then the grid-wide sweeps
       for (int row = r0 + tid; row < r1; row += NT) p.z[row] = row_dot(Vt, row);
       CYCLE_SYNC();
-      if (!pc_apply_grid(s_pc, p.z, 1, 0, cycle_sync)) {
+      if (!pc_apply_grid<GPC>(s_pc, p.z, 1, 0, cycle_sync)) {
         cycle_abort();
         return;
       }
@@ -1996,7 +1997,7 @@ __global__ void __launch_bounds__(NT, SKR_CYCLE_MINB) k_cycle(Ptrs p, int cycle_
   }
   if (GPC) {
     CYCLE_SYNC();
-    if (!pc_apply_grid(s_pc, p.r, 1, 0, cycle_sync)) {
+    if (!pc_apply_grid<GPC>(s_pc, p.r, 1, 0, cycle_sync)) {
       cycle_abort();
       return;
     }
@@ -2574,10 +2575,11 @@ static std::mutex g_mu;
 // k_cycle instantiation for R rows per lane (1, 2 or 4)
 static const void* cycle_kernel(int R) {
   switch (R) {
-    case 1: return (const void*)k_cycle<1, false>;
-    case 2: return (const void*)k_cycle<2, false>;
-    case 4: return (const void*)k_cycle<4, false>;
-    default: return (const void*)k_cycle<2, true>;  // general preconditioner
+    case 1: return (const void*)k_cycle<1, 0>;
+    case 2: return (const void*)k_cycle<2, 0>;
+    case 4: return (const void*)k_cycle<4, 0>;
+    case 8: return (const void*)k_cycle<2, 1>;   // general preconditioner, triangular kinds
+    default: return (const void*)k_cycle<2, 2>;  // block Jacobi
   }
 }
 
@@ -2608,7 +2610,7 @@ static int ensure_dev(DevInfo** out) {
                              (int)dense_smem_bytes()) != cudaSuccess)
       return SKR_ERR_CUDA;
     int nb = 1 << 30;
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 5; ++v) {
       const void* f = cycle_kernel(1 << v);
       if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)CYCLE_DSMEM_BUDGET) != cudaSuccess)
@@ -2924,7 +2926,20 @@ int skr_gcrodr_solve(const skr_csr* A, const double* b, const double* x0, double
   const size_t upd_smem =
       (SL.cmb + 2 * (size_t)((L.kcap + 7) / 8 * 8) * comb_ld(cfg->m)) * sizeof(double);
   int csr_cap_i = (int)csr_cap;
-  const void* cycle_fn = cycle_kernel(p.pch ? 8 : cycle_rows_per_lane(p.rpb));
+  int pc_family = 0;  // 1 triangular, 2 block Jacobi
+  if (p.pch) {
+    pc_family = A->precond_kind == SKR_PC_BJACOBI ? 2 : A->precond_kind > 0 ? 1 : 0;
+    if (!pc_family) {  // kind not given: read it from the buffer's header
+      int hk = 0;
+      if (cudaMemcpyAsync(&hk, &p.pch->v.kind, sizeof(int), cudaMemcpyDeviceToHost, s) !=
+              cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        return SKR_ERR_CUDA;
+      pc_family = hk == PC_BJACOBI ? 2 : 1;
+    }
+  }
+  const void* cycle_fn =
+      cycle_kernel(pc_family ? 8 * pc_family : cycle_rows_per_lane(p.rpb));
   int pc_target = 0, pc_stage = 0;
   void* pcargs[3] = {&p, &pc_target, &pc_stage};
   auto launch_pc = [&](int target, int stage) {

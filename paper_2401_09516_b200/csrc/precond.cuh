@@ -181,9 +181,13 @@ __device__ __forceinline__ bool pc_tri_sweep(const PcView& pc, int s, double* v,
 
 // Block Jacobi: block b's slice of every column <- U^-1 L^-1 P (slice), one
 // warp per (block, column); RB = ceil(bs / 32) entries per lane in registers.
+// The factor's columns stream through registers D columns ahead of the
+// substitution step that uses them (they do not depend on the solution), so
+// the sequential steps do not each wait for their own memory round trip.
 template <int RB>
 __device__ __forceinline__ void pc_block_solve(const PcView& pc, double* v, int ncols, size_t ldv,
                                                int n) {
+  constexpr int D = RB <= 2 ? 8 : 1;  // columns in flight (blocks of up to 64 rows: 8)
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -200,34 +204,70 @@ __device__ __forceinline__ void pc_block_solve(const PcView& pc, double* v, int 
       x[r] = i < bsz ? col[start + __ldg(pc.perm + start + i)] : 0.0;
     }
     __syncwarp();  // every gather is done before the slice is overwritten
+    double cur[D][RB], nxt[D][RB];
+    auto load_chunk = [&](double (&dst)[D][RB], int k0) {  // columns k0 .. k0 + D - 1
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int i = 32 * r + lane, k = k0 + d;
+          dst[d][r] = (k >= 0 && k < bsz && i < bsz) ? __ldg(lu + i + (size_t)k * bs) : 0.0;
+        }
+    };
+    auto x_at = [&](int k) -> double {  // x[k] of the block, broadcast
+      double src = x[0];
+#pragma unroll
+      for (int r = 1; r < RB; ++r)
+        if (r == (k >> 5)) src = x[r];
+      return __shfl_sync(0xffffffffu, src, k & 31);
+    };
     // forward, unit lower
+    load_chunk(nxt, 0);
+    for (int k0 = 0; k0 < bsz; k0 += D) {
 #pragma unroll
-    for (int r = 0; r < RB; ++r)
-      for (int kl = 0; kl < 32; ++kl) {
-        const int k = 32 * r + kl;
-        if (k >= bsz) break;
-        const double xk = __shfl_sync(0xffffffffu, x[r], kl);
+      for (int d = 0; d < D; ++d)
 #pragma unroll
-        for (int r2 = r; r2 < RB; ++r2) {
-          const int i = 32 * r2 + lane;
-          if (i > k && i < bsz)
-            x[r2] = __dsub_rn(x[r2], __dmul_rn(__ldg(lu + i + (size_t)k * bs), xk));
+        for (int r = 0; r < RB; ++r) cur[d][r] = nxt[d][r];
+      if (k0 + D < bsz) load_chunk(nxt, k0 + D);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int k = k0 + d;
+        if (k < bsz) {
+          const double xk = x_at(k);
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            const int i = 32 * r + lane;
+            if (i > k && i < bsz) x[r] = __dsub_rn(x[r], __dmul_rn(cur[d][r], xk));
+          }
         }
       }
-    // backward, upper
+    }
+    // backward, upper: chunks of columns from the last one down
+    const int klast = ((bsz - 1) / D) * D;
+    load_chunk(nxt, klast);
+    for (int k0 = klast; k0 >= 0; k0 -= D) {
 #pragma unroll
-    for (int r = RB - 1; r >= 0; --r)
-      for (int kl = 31; kl >= 0; --kl) {
-        const int k = 32 * r + kl;
-        if (k >= bsz) continue;
-        if (lane == kl) x[r] = __ddiv_rn(x[r], __ldg(lu + k + (size_t)k * bs));
-        const double xk = __shfl_sync(0xffffffffu, x[r], kl);
+      for (int d = 0; d < D; ++d)
 #pragma unroll
-        for (int r2 = 0; r2 <= r; ++r2) {
-          const int i = 32 * r2 + lane;
-          if (i < k) x[r2] = __dsub_rn(x[r2], __dmul_rn(__ldg(lu + i + (size_t)k * bs), xk));
+        for (int r = 0; r < RB; ++r) cur[d][r] = nxt[d][r];
+      if (k0 - D >= 0) load_chunk(nxt, k0 - D);
+#pragma unroll
+      for (int d = D - 1; d >= 0; --d) {
+        const int k = k0 + d;
+        if (k < bsz) {
+          // the diagonal entry lives in the lane that owns row k
+#pragma unroll
+          for (int r = 0; r < RB; ++r)
+            if (r == (k >> 5) && lane == (k & 31)) x[r] = __ddiv_rn(x[r], cur[d][r]);
+          const double xk = x_at(k);
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            const int i = 32 * r + lane;
+            if (i < k) x[r] = __dsub_rn(x[r], __dmul_rn(cur[d][r], xk));
+          }
         }
       }
+    }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       const int i = 32 * r + lane;
@@ -239,11 +279,14 @@ __device__ __forceinline__ void pc_block_solve(const PcView& pc, double* v, int 
 // v[:, c] <- M^-1 v[:, c] for c < ncols, by every CTA of a cooperative grid.
 // The caller has made v visible grid-wide (a barrier after it was written);
 // on return (true) the result is visible grid-wide as well.
-template <class Sync>
+// FAMILY: 1 = triangular kinds only, 2 = block Jacobi only (the cycle kernel
+// is instantiated per family so that neither's registers crowd the other),
+// 0 = either (standalone kernels, run-time dispatch).
+template <int FAMILY = 0, class Sync>
 __device__ __forceinline__ bool pc_apply_grid(const PcView& pc, double* v, int ncols, size_t ldv,
                                               Sync&& sync) {
   const int n = pc.n;
-  if (pc.kind == PC_BJACOBI) {
+  if (FAMILY == 2 || (FAMILY == 0 && pc.kind == PC_BJACOBI)) {
     if (pc.bs <= 32)
       pc_block_solve<1>(pc, v, ncols, ldv, n);
     else if (pc.bs <= 64)

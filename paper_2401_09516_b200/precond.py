@@ -224,7 +224,7 @@ def build_device_preconditioner(dA: DeviceCsr, kind: str, *, sor_omega: float = 
     info = (ctypes.c_int32 * 2)(0, 0)
     val = ctypes.c_double(0.0)
     plain = _lib.SkrCsr(dA.n, dA.nnz, dA.row_ptr.data_ptr(), dA.col_idx.data_ptr(),
-                        dA.values.data_ptr(), None, None, 0, 0, None)
+                        dA.values.data_ptr(), None, None, 0, 0, None, 0)
     _lib.check(L.skr_precond_build(ctypes.byref(plain), kid, omega, bs, buf.data_ptr(), nbytes,
                                    info if check else None,
                                    ctypes.byref(val) if check else None,

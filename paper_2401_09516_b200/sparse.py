@@ -158,7 +158,8 @@ class DeviceCsr:
                              col_idx.data_ptr(), values.data_ptr(),
                              diag.data_ptr() if diag is not None else None,
                              buf.data_ptr() if buf is not None else None, int(sx), int(sxy),
-                             precond.buffer.data_ptr() if precond is not None else None)
+                             precond.buffer.data_ptr() if precond is not None else None,
+                             _lib.PC_KINDS.get(getattr(precond, "kind", ""), 0))
 
     def stencil_active(self) -> bool:
         """True when the device check accepted the stencil form (syncs)."""
@@ -178,7 +179,7 @@ class DeviceCsr:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=self.values.device)
         probe = _lib.SkrCsr(self.n, int(self.values.numel()), self.row_ptr.data_ptr(),
                             self.col_idx.data_ptr(), self.values.data_ptr(), None, None, 0, 0,
-                            None)
+                            None, 0)
         _lib.check(L.skr_stencil_build(ctypes.byref(probe), sx, sxy, buf.data_ptr(), nbytes,
                                        _lib.stream_handle(stream)), "skr_stencil_build")
         return DeviceCsr(self.n, self.row_ptr, self.col_idx, self.values, self.diag, self._keep,
